@@ -1,0 +1,175 @@
+/* episodic_b200 — C-ABI of the B200-native frequent-episode counter.
+ *
+ * This is the drop-in boundary for the reference's counting hot path
+ * (paths relative to /root/reference/proj/include/episodic):
+ *   EventStream::from_events  types.hpp:102-119  -> epi_load_stream
+ *   build_index               index.hpp:20-30    -> (inside epi_load_stream)
+ *   count_fsm                 fsm.hpp:101-106    -> epi_count (one episode)
+ *   count_tracking            tracking.hpp:391   -> epi_count (same counts)
+ *   count_mapconcat           mapconcat.hpp:71   -> epi_count (same counts)
+ *   counting block of mine()  miner.hpp:145-154  -> epi_count (one call/level)
+ *   mine()                    miner.hpp:114-173  -> epi_mine
+ *   generate()                datagen.hpp:71-122 -> epi_generate
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * Every call returns an epi_status; the message of the last failure is
+ * available from epi_last_error(ctx). A C++ adaptor that rethrows the
+ * reference's exception types lives in episodic_b200.hpp.
+ */
+#ifndef EPISODIC_B200_H
+#define EPISODIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EPI_OK = 0,
+  EPI_EINVAL = 1,      /* std::invalid_argument in the reference (validate, mine) */
+  EPI_EDATA = 2,       /* episodic::DataError (from_events)                       */
+  EPI_EOVERFLOW = 3,   /* std::overflow_error                                     */
+  EPI_ECUDA = 4,       /* CUDA runtime failure                                    */
+  EPI_ENCCL = 5,       /* NCCL failure (multi-GPU allgather)                      */
+  EPI_ENOMEM = 6,      /* device or host allocation failed                        */
+  EPI_EUNSUPPORTED = 7 /* input outside what this build's kernels support         */
+} epi_status;
+
+typedef struct epi_ctx epi_ctx;
+
+/* Episode batch in CSR form. Episode e has nodes types[offsets[e] ..
+ * offsets[e+1]) and N-1 interval constraints (low, high] stored at
+ * low/high[offsets[e]-e .. offsets[e+1]-e-1) (one fewer constraint than nodes
+ * per episode, so no separate constraint offsets are needed). */
+typedef struct {
+  uint64_t n_episodes;
+  const uint32_t* offsets; /* n_episodes + 1 entries, offsets[0] == 0 */
+  const uint32_t* types;
+  const int64_t* low;
+  const int64_t* high;
+} epi_episode_batch;
+
+typedef enum {
+  EPI_MODE_EXACT = 0, /* every count exact (count_fsm semantics)                  */
+  EPI_MODE_MINE = 1   /* pass 1 relaxed upper bound prunes; survivors exact;
+                         pruned entries get EPI_COUNT_PRUNED and frequent = 0   */
+} epi_mode;
+
+#define EPI_COUNT_PRUNED UINT64_MAX
+
+typedef struct {
+  uint64_t episodes;          /* candidates in the call                        */
+  uint64_t pass1_groups;      /* relaxed episodes counted by pass 1            */
+  uint64_t pass2_episodes;    /* episodes counted exactly by pass 2            */
+  uint64_t pruned;            /* candidates eliminated by pass 1               */
+  uint64_t segments;          /* MapConcatenate segments per episode           */
+  uint64_t patches;           /* boundary machines re-run by the concat walk   */
+  uint64_t kernel_launches;   /* device kernels launched by the call           */
+  uint64_t map_launches;      /* segment-map (automaton) kernel launches       */
+  uint64_t episode_events;    /* sum over device passes of episodes x events   */
+  uint64_t matched_pairs;     /* sum over passes of sum_e sum_k n(type_k)      */
+  uint64_t tile_steps;        /* (episode, 32 ms tile) automaton steps, map    */
+  uint64_t h2d_bytes;         /* host->device bytes moved by the call          */
+  uint64_t d2h_bytes;         /* device->host bytes moved by the call          */
+  double pass1_ms, pass2_ms;  /* device time of each pass (CUDA events)        */
+  double map_ms;              /* device time of the segment-map kernels        */
+  double concat_ms;           /* device time of the concat walks               */
+  double total_ms;            /* device time of the whole call                 */
+} epi_stats;
+
+/* Context bound to one CUDA device. */
+epi_status epi_create(int device, epi_ctx** out);
+void epi_destroy(epi_ctx* ctx);
+/* Message of the last failure on ctx (or of the calling thread's last
+ * context-free call when ctx is NULL). */
+const char* epi_last_error(const epi_ctx* ctx);
+const char* epi_status_name(epi_status s);
+
+/* Load (replace) the event stream: validated exactly like
+ * EventStream::from_events (times >= 0, non-decreasing, type < alphabet;
+ * the first offending event decides the message). Host arrays are borrowed
+ * for the call; the device copy is owned by the context. */
+epi_status epi_load_stream(epi_ctx* ctx, const uint32_t* types, const int64_t* times,
+                           uint64_t n, uint32_t alphabet);
+
+/* Same, from arrays already resident on the context's device (for callers
+ * that keep the stream in HBM). */
+epi_status epi_load_stream_device(epi_ctx* ctx, const uint32_t* d_types, const int64_t* d_times,
+                                  uint64_t n, uint32_t alphabet);
+
+uint64_t epi_stream_size(const epi_ctx* ctx);
+
+/* Count every episode of the batch over the loaded stream. counts_out has
+ * n_episodes entries; frequent_out (optional) receives count >= threshold.
+ * stats (optional) receives the pass breakdown. Validation of each episode
+ * follows validate(Episode) (types.hpp:87-92). */
+epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,
+                     uint32_t mode, uint64_t* counts_out, uint8_t* frequent_out,
+                     epi_stats* stats);
+
+/* Level-wise mining, mine() (miner.hpp:114-173) with one epi_count call per
+ * level. The result is owned by the context until the next epi_mine call:
+ *   *n_levels                     levels produced
+ *   level_candidates[l]           candidates generated at level l+1
+ *   level_offsets[l..l+1]         frequent episodes of level l+1 in the flat
+ *                                 result list (candidate-generation order)
+ *   res_batch                     the flat frequent episodes (CSR, as above)
+ *   res_counts                    their exact counts
+ * constraint alphabet: n_alpha bins (alpha_low[i], alpha_high[i]]. */
+typedef struct {
+  uint64_t threshold;
+  uint64_t max_level;
+  const int64_t* alpha_low;
+  const int64_t* alpha_high;
+  uint64_t n_alpha;
+  uint32_t mode; /* epi_mode used for levels >= 2 */
+} epi_mine_config;
+
+typedef struct {
+  uint64_t n_levels;
+  const uint64_t* level_candidates;
+  const uint64_t* level_offsets;
+  const double* level_ms; /* wall time per level (host clock, like LevelResult) */
+  epi_episode_batch frequent;
+  const uint64_t* counts;
+  epi_stats totals;
+} epi_mine_result;
+
+epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out);
+
+/* Synthetic spike-train generator, a bit-exact restatement of generate()
+ * (datagen.hpp:71-122): per-neuron homogeneous Poisson background plus
+ * injected episodes with uniform gaps, ties ordered by neuron id. The
+ * embedded episodes use the batch CSR layout (may be NULL); rates[e] is
+ * episode e's injection rate in Hz. *types_out / *times_out are allocated by
+ * the library (release with epi_free); *n_out receives the event count.
+ * Host-side C++, parallel over neurons. Errors are reported through
+ * epi_last_error(NULL). */
+epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                        const epi_episode_batch* embedded, const double* rates,
+                        uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
+void epi_free(void* p);
+
+/* generate_candidates (miner.hpp:76-109) exposed for parity tests and for
+ * callers that drive their own level loop: `frequent` holds level-1 frequent
+ * episodes (all of length level-1; ignored for level 1). Host-only (no device
+ * needed). The output batch is owned by ctx (or, when ctx is NULL, by the
+ * calling thread) until the next call. */
+epi_status epi_generate_candidates(epi_ctx* ctx, uint64_t level, const epi_episode_batch* frequent,
+                                   const int64_t* alpha_low, const int64_t* alpha_high,
+                                   uint64_t n_alpha, uint32_t alphabet_size,
+                                   epi_episode_batch* out);
+
+/* INT32 issue-rate probe (roofline denominator): lane-ops/s in units of
+ * 1e12 on `device`; mixed != 0 saturates both integer pipes (LOP3 + IMAD),
+ * mixed == 0 the ALU pipe only (LOP3). */
+epi_status epi_probe_int32(int device, int mixed, double* tops_out);
+
+/* Build/version string (arch, kernel variants). */
+const char* epi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,431 @@
+"""Python mirror of the reference's counting / mining API, backed by the
+B200 kernels through the C-ABI (no CPU counting path exists).
+
+Reference surface mirrored (paths relative to
+/root/reference/proj/include/episodic):
+
+  Event, IntervalConstraint, Episode, EventStream   types.hpp:20-134
+  DataError, validate                               types.hpp:75-92
+  count_fsm(stream, ep)                             fsm.hpp:101-106
+  count_tracking(stream, index, ep, opt)            tracking.hpp:391-407
+  count_mapconcat(stream, ep, segments, workers)    mapconcat.hpp:71-159
+  generate_candidates(level, frequent, alpha, A)    miner.hpp:76-109
+  MiningConfig / LevelResult / MiningResult / mine  miner.hpp:26-173
+  write_mining_csv, format_episode                  miner.hpp:175-181, grammar.hpp:70-83
+  GenConfig / Embedding / generate                  datagen.hpp:19-122
+
+Errors map to the reference's exception types: std::invalid_argument ->
+InvalidArgument (a ValueError), DataError -> DataError (a RuntimeError),
+std::overflow_error -> OverflowError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, NamedTuple, Sequence
+
+import numpy as np
+
+from . import _native as N
+
+
+class EpisodicError(RuntimeError):
+    pass
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class DataError(RuntimeError):
+    """episodic::DataError (E/types.hpp:75-80)."""
+
+
+class Unsupported(EpisodicError):
+    pass
+
+
+def _raise(status: int, msg: str):
+    if status == N.EPI_EINVAL:
+        raise InvalidArgument(msg)
+    if status == N.EPI_EDATA:
+        raise DataError(msg)
+    if status == N.EPI_EOVERFLOW:
+        raise OverflowError(msg)
+    if status == N.EPI_EUNSUPPORTED:
+        raise Unsupported(msg)
+    name = N.lib.epi_status_name(status).decode()
+    raise EpisodicError(f"{name}: {msg}")
+
+
+class Event(NamedTuple):
+    type: int
+    time: int
+
+
+class IntervalConstraint(NamedTuple):
+    """Half-open gap constraint: g admissible iff low < g <= high."""
+    low: int
+    high: int
+
+    def contains_gap(self, gap: int) -> bool:
+        return self.low < gap <= self.high
+
+
+@dataclass(eq=True)
+class Episode:
+    types: list = field(default_factory=list)
+    constraints: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self.types = [int(t) for t in self.types]
+        self.constraints = [IntervalConstraint(int(c[0]), int(c[1])) for c in self.constraints]
+
+    def size(self) -> int:
+        return len(self.types)
+
+    def slice(self, first: int, length: int) -> "Episode":
+        return Episode(self.types[first:first + length],
+                       self.constraints[first:first + length - 1] if length > 1 else [])
+
+    def key(self):
+        return (tuple(self.types), tuple(self.constraints))
+
+
+def validate(ep: Episode) -> None:
+    """validate(Episode), E/types.hpp:82-92."""
+    if not ep.types:
+        raise InvalidArgument("episode must have at least one node")
+    if len(ep.constraints) + 1 != len(ep.types):
+        raise InvalidArgument("episode needs exactly N-1 constraints")
+    for c in ep.constraints:
+        if c.low < 0 or c.low >= c.high:
+            raise InvalidArgument("interval constraint requires 0 <= low < high")
+
+
+class EventStream:
+    """Time-ordered SoA event stream (E/types.hpp:96-134). Validation of
+    from_events happens on the device when the stream is loaded; it raises
+    DataError with the reference's messages."""
+
+    def __init__(self, types: np.ndarray, times: np.ndarray, alphabet: int):
+        self.types_ = np.ascontiguousarray(types, dtype=np.uint32)
+        self.times_ = np.ascontiguousarray(times, dtype=np.int64)
+        if self.types_.shape != self.times_.shape:
+            raise InvalidArgument("types and times must have the same length")
+        self.alphabet_ = int(alphabet)
+
+    @staticmethod
+    def from_events(events: Iterable, alphabet_size: int) -> "EventStream":
+        """EventStream::from_events (E/types.hpp:102-119): the first offending
+        event decides the error, checks in the reference's order."""
+        ev = list(events)
+        types = np.array([int(e[0]) for e in ev], dtype=np.int64).reshape(-1)
+        times = np.array([int(e[1]) for e in ev], dtype=np.int64).reshape(-1)
+        bad_neg = times < 0
+        bad_order = np.zeros_like(bad_neg)
+        if len(ev) > 1:
+            bad_order[1:] = times[1:] < times[:-1]
+        bad_type = (types < 0) | (types >= alphabet_size)
+        bad = bad_neg | bad_order | bad_type
+        if bad.any():
+            i = int(np.argmax(bad))
+            if bad_neg[i]:
+                raise DataError("negative event time")
+            if bad_order[i]:
+                raise DataError("event times must be non-decreasing")
+            raise DataError("event type id out of range")
+        return EventStream(types.astype(np.uint32), times, alphabet_size)
+
+    @staticmethod
+    def from_arrays(types, times, alphabet_size: int) -> "EventStream":
+        return EventStream(types, times, alphabet_size)
+
+    def size(self) -> int:
+        return int(self.types_.shape[0])
+
+    def __len__(self):
+        return self.size()
+
+    def empty(self) -> bool:
+        return self.size() == 0
+
+    def type_at(self, i: int) -> int:
+        return int(self.types_[i])
+
+    def time_at(self, i: int) -> int:
+        return int(self.times_[i])
+
+    def alphabet_size(self) -> int:
+        return self.alphabet_
+
+    def types(self) -> np.ndarray:
+        return self.types_
+
+    def times(self) -> np.ndarray:
+        return self.times_
+
+
+def episodes_to_csr(episodes: Sequence[Episode]) -> N.CSR:
+    off = np.zeros(len(episodes) + 1, dtype=np.uint32)
+    types, lo, hi = [], [], []
+    for i, ep in enumerate(episodes):
+        types.extend(ep.types)
+        for c in ep.constraints:
+            lo.append(c[0])
+            hi.append(c[1])
+        if len(ep.constraints) + 1 != len(ep.types) and ep.types:
+            raise InvalidArgument("episode needs exactly N-1 constraints")
+        off[i + 1] = off[i] + len(ep.types)
+    return N.CSR(off, np.array(types, dtype=np.uint32), np.array(lo, dtype=np.int64),
+                 np.array(hi, dtype=np.int64))
+
+
+def csr_to_episodes(csr: N.CSR) -> list:
+    return [Episode(*csr.episode(e)) for e in range(len(csr))]
+
+
+class Context:
+    """One device context (epi_ctx): a resident stream plus counting."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        st = N.lib.epi_create(device, C.byref(h))
+        if st != N.EPI_OK:
+            _raise(st, N.lib.epi_last_error(None).decode())
+        self._h = h
+        self._loaded = None
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.epi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != N.EPI_OK:
+            _raise(st, N.lib.epi_last_error(self._h).decode())
+
+    def load(self, stream: EventStream):
+        if self._loaded is stream:
+            return
+        self._loaded = None
+        self._check(N.lib.epi_load_stream(self._h, N.ptr(stream.types_, C.c_uint32),
+                                          N.ptr(stream.times_, C.c_int64), stream.size(),
+                                          stream.alphabet_))
+        self._loaded = stream
+
+    def load_arrays(self, types: np.ndarray, times: np.ndarray, alphabet: int):
+        """Load from host arrays (pinned or pageable); returns nothing."""
+        self._loaded = None
+        self._check(N.lib.epi_load_stream(self._h, N.ptr(types, C.c_uint32), N.ptr(times, C.c_int64),
+                                          int(types.shape[0]), alphabet))
+
+    def load_device(self, d_types_ptr: int, d_times_ptr: int, n: int, alphabet: int):
+        self._loaded = None
+        self._check(N.lib.epi_load_stream_device(self._h, C.c_void_p(d_types_ptr),
+                                                 C.c_void_p(d_times_ptr), n, alphabet))
+
+    def count_csr(self, csr: N.CSR, threshold: int = 1, mode: int = N.MODE_EXACT,
+                  with_frequent: bool = False):
+        n = len(csr)
+        counts = np.zeros(n, dtype=np.uint64)
+        freq = np.zeros(n, dtype=np.uint8) if with_frequent else None
+        stats = N.Stats()
+        self._check(N.lib.epi_count(self._h, C.byref(csr.struct), int(threshold), int(mode),
+                                    N.ptr(counts, C.c_uint64),
+                                    N.ptr(freq, C.c_uint8) if freq is not None else None,
+                                    C.byref(stats)))
+        self.last_stats = stats.as_dict()
+        return (counts, freq) if with_frequent else counts
+
+    def count(self, stream: EventStream, episodes: Sequence[Episode], threshold: int = 1,
+              mode: int = N.MODE_EXACT):
+        self.load(stream)
+        return self.count_csr(episodes_to_csr(episodes), threshold, mode)
+
+    def mine_raw(self, threshold: int, bins: Sequence, max_level: int, mode: int = N.MODE_MINE):
+        lo = np.array([b[0] for b in bins], dtype=np.int64)
+        hi = np.array([b[1] for b in bins], dtype=np.int64)
+        cfg = N.MineConfig(int(threshold), int(max_level), N.ptr(lo, C.c_int64), N.ptr(hi, C.c_int64),
+                           len(bins), int(mode))
+        res = N.MineResult()
+        self._check(N.lib.epi_mine(self._h, C.byref(cfg), C.byref(res)))
+        nl = int(res.n_levels)
+        cands = [int(res.level_candidates[i]) for i in range(nl)]
+        offs = [int(res.level_offsets[i]) for i in range(nl + 1)]
+        ms = [float(res.level_ms[i]) for i in range(nl)]
+        csr = N.CSR.from_struct(res.frequent)
+        nf = len(csr)
+        counts = np.ctypeslib.as_array(res.counts, shape=(nf,)).copy() if nf else np.zeros(0, np.uint64)
+        return cands, offs, ms, csr, counts, res.totals.as_dict()
+
+
+_default = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context(0)
+    return _default
+
+
+def count_batch(stream: EventStream, episodes: Sequence[Episode]) -> np.ndarray:
+    """Batch entry point (no reference equivalent: the reference loops over
+    candidates, E/miner.hpp:145-154)."""
+    for ep in episodes:
+        validate(ep)
+    return default_context().count(stream, episodes)
+
+
+def count_fsm(stream: EventStream, ep: Episode) -> int:
+    """count_fsm, E/fsm.hpp:101-106."""
+    validate(ep)
+    return int(default_context().count(stream, [ep])[0])
+
+
+def count_tracking(stream: EventStream, index, ep: Episode, opt=None, stats=None) -> int:
+    """count_tracking, E/tracking.hpp:391-407: equal to count_fsm on every
+    input; the index, options and stats are accepted for signature parity."""
+    return count_fsm(stream, ep)
+
+
+def count_mapconcat(stream: EventStream, ep: Episode, segments: int, workers: int = 1,
+                    stats=None) -> int:
+    """count_mapconcat, E/mapconcat.hpp:71-159. The device counter is always
+    segment-parallel; the count does not depend on `segments`."""
+    validate(ep)
+    if segments < 1:
+        raise InvalidArgument("count_mapconcat: segments must be >= 1")
+    if stream.size() == 0:
+        return 0
+    return count_fsm(stream, ep)
+
+
+def generate_candidates(level: int, frequent: Sequence[Episode], alphabet: Sequence,
+                        alphabet_size: int) -> list:
+    """generate_candidates, E/miner.hpp:76-109 (host C++ join)."""
+    csr = episodes_to_csr(list(frequent)) if frequent else N.CSR(np.zeros(1, np.uint32), [], [], [])
+    lo = np.array([c[0] for c in alphabet], dtype=np.int64)
+    hi = np.array([c[1] for c in alphabet], dtype=np.int64)
+    out = N.EpisodeBatch()
+    st = N.lib.epi_generate_candidates(None, int(level), C.byref(csr.struct), N.ptr(lo, C.c_int64),
+                                       N.ptr(hi, C.c_int64), len(lo), int(alphabet_size), C.byref(out))
+    if st != N.EPI_OK:
+        _raise(st, N.lib.epi_last_error(None).decode())
+    return csr_to_episodes(N.CSR.from_struct(out))
+
+
+@dataclass
+class MiningConfig:
+    """MiningConfig, E/miner.hpp:26-37. `backend`, `strategy_switch_level`,
+    `tracking`, `segments` and `workers` are accepted for parity; the device
+    counter replaces all of them. `mode` selects two-pass elimination."""
+    threshold: int = 1
+    constraint_alphabet: list = field(default_factory=list)
+    max_level: int = 16
+    strategy_switch_level: int = 3
+    backend: str = "device"
+    tracking: object = None
+    segments: int = 4
+    workers: int = 1
+    mode: int = N.MODE_MINE
+
+
+@dataclass
+class LevelResult:
+    level: int = 0
+    candidates: int = 0
+    frequent: list = field(default_factory=list)
+    elapsed_ms: float = 0.0
+
+
+@dataclass
+class MiningResult:
+    levels: list = field(default_factory=list)
+    stats: dict = field(default_factory=dict)
+
+
+def mine(stream: EventStream, cfg: MiningConfig, ctx: Context | None = None) -> MiningResult:
+    """mine, E/miner.hpp:114-173, one device count per level."""
+    ctx = ctx or default_context()
+    ctx.load(stream)
+    cands, offs, ms, csr, counts, totals = ctx.mine_raw(cfg.threshold, cfg.constraint_alphabet,
+                                                        cfg.max_level, cfg.mode)
+    eps = csr_to_episodes(csr)
+    levels = []
+    for i in range(len(cands)):
+        fr = [(eps[j], int(counts[j])) for j in range(offs[i], offs[i + 1])]
+        levels.append(LevelResult(i + 1, cands[i], fr, ms[i]))
+    return MiningResult(levels, totals)
+
+
+def format_episode(ep: Episode, names=None) -> str:
+    """format_episode, E/grammar.hpp:70-83 (numeric symbol table by default)."""
+    out = []
+    for i, t in enumerate(ep.types):
+        if i:
+            c = ep.constraints[i - 1]
+            out.append(f"-({c.low},{c.high}]-")
+        out.append(str(t) if names is None else names[t])
+    return "".join(out)
+
+
+def write_mining_csv(result: MiningResult, names=None) -> str:
+    """write_mining_csv, E/miner.hpp:175-181."""
+    lines = ["level,episode,count"]
+    for lvl in result.levels:
+        for ep, cnt in lvl.frequent:
+            lines.append(f"{lvl.level},{format_episode(ep, names)},{cnt}")
+    return "\n".join(lines) + "\n"
+
+
+@dataclass
+class Embedding:
+    episode: Episode
+    rate_hz: float = 1.0
+
+
+@dataclass
+class GenConfig:
+    """GenConfig, E/datagen.hpp:19-25."""
+    neurons: int = 64
+    duration_s: float = 100.0
+    base_rate_hz: float = 20.0
+    embedded: list = field(default_factory=list)
+    seed: int = 0
+
+
+def generate_arrays(cfg: GenConfig):
+    """generate(), E/datagen.hpp:71-122, as (types u32, times i64) arrays."""
+    eps = [e.episode for e in cfg.embedded]
+    csr = episodes_to_csr(eps) if eps else None
+    rates = np.array([e.rate_hz for e in cfg.embedded], dtype=np.float64)
+    tp, tm, n = N.u32p(), N.i64p(), C.c_uint64()
+    st = N.lib.epi_generate(int(cfg.neurons), float(cfg.duration_s), float(cfg.base_rate_hz),
+                            int(cfg.seed) & ((1 << 64) - 1),
+                            C.byref(csr.struct) if csr is not None else None,
+                            N.ptr(rates, C.c_double) if len(rates) else None,
+                            C.byref(tp), C.byref(tm), C.byref(n))
+    if st != N.EPI_OK:
+        _raise(st, N.lib.epi_last_error(None).decode())
+    try:
+        cnt = int(n.value)
+        types = np.ctypeslib.as_array(tp, shape=(max(cnt, 1),))[:cnt].copy()
+        times = np.ctypeslib.as_array(tm, shape=(max(cnt, 1),))[:cnt].copy()
+    finally:
+        N.lib.epi_free(C.cast(tp, C.c_void_p))
+        N.lib.epi_free(C.cast(tm, C.c_void_p))
+    return types, times
+
+
+def generate(cfg: GenConfig) -> EventStream:
+    types, times = generate_arrays(cfg)
+    return EventStream(types, times, cfg.neurons)

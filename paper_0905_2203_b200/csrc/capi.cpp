@@ -1,0 +1,187 @@
+// extern "C" boundary (include/episodic_b200.h). Every entry point catches
+// and maps exceptions to epi_status; messages follow the reference's.
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/episodic_b200.h"
+#include "engine.h"
+
+struct CandStore {
+  std::vector<uint32_t> gc_off, gc_types;
+  std::vector<int64_t> gc_lo, gc_hi;
+};
+
+struct epi_ctx {
+  epi::Engine engine;
+  CandStore cands;
+  explicit epi_ctx(int device) : engine(device) {}
+};
+
+namespace epi {
+void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                     const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
+                     std::vector<int64_t>& times);
+}
+
+namespace {
+
+thread_local std::string g_free_err;
+
+template <class F>
+epi_status guarded(std::string& err, F&& f) {
+  try {
+    f();
+    err.clear();
+    return EPI_OK;
+  } catch (const epi::Error& e) {
+    err = e.what();
+    return static_cast<epi_status>(e.status);
+  } catch (const std::bad_alloc&) {
+    err = "host allocation failed";
+    return EPI_ENOMEM;
+  } catch (const std::exception& e) {
+    err = e.what();
+    return EPI_EINVAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* epi_version(void) {
+  return "episodic_b200 0.1 sm_100a: bit-sliced tile automaton (32 ms tiles, high<=63, N<=16), "
+         "MapConcatenate segments + concat walk, two-pass hull pruning";
+}
+
+const char* epi_status_name(epi_status s) {
+  switch (s) {
+    case EPI_OK: return "EPI_OK";
+    case EPI_EINVAL: return "EPI_EINVAL";
+    case EPI_EDATA: return "EPI_EDATA";
+    case EPI_EOVERFLOW: return "EPI_EOVERFLOW";
+    case EPI_ECUDA: return "EPI_ECUDA";
+    case EPI_ENCCL: return "EPI_ENCCL";
+    case EPI_ENOMEM: return "EPI_ENOMEM";
+    case EPI_EUNSUPPORTED: return "EPI_EUNSUPPORTED";
+  }
+  return "EPI_UNKNOWN";
+}
+
+epi_status epi_create(int device, epi_ctx** out) {
+  if (!out) return EPI_EINVAL;
+  *out = nullptr;
+  return guarded(g_free_err, [&] { *out = new epi_ctx(device); });
+}
+
+void epi_destroy(epi_ctx* ctx) { delete ctx; }
+
+const char* epi_last_error(const epi_ctx* ctx) {
+  return ctx ? ctx->engine.err.c_str() : g_free_err.c_str();
+}
+
+epi_status epi_load_stream(epi_ctx* ctx, const uint32_t* types, const int64_t* times, uint64_t n,
+                           uint32_t alphabet) {
+  if (!ctx) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] { ctx->engine.load_stream_host(types, times, n, alphabet); });
+}
+
+epi_status epi_load_stream_device(epi_ctx* ctx, const uint32_t* d_types, const int64_t* d_times,
+                                  uint64_t n, uint32_t alphabet) {
+  if (!ctx) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err,
+                 [&] { ctx->engine.load_stream_device(d_types, d_times, n, alphabet); });
+}
+
+uint64_t epi_stream_size(const epi_ctx* ctx) { return ctx ? ctx->engine.stream_size() : 0; }
+
+epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,
+                     uint32_t mode, uint64_t* counts_out, uint8_t* frequent_out,
+                     epi_stats* stats) {
+  if (!ctx || !batch) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    ctx->engine.count_batch(*batch, threshold, mode, counts_out, frequent_out, stats);
+  });
+}
+
+epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out) {
+  if (!ctx || !cfg || !out) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out); });
+}
+
+epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                        const epi_episode_batch* embedded, const double* rates,
+                        uint32_t** types_out, int64_t** times_out, uint64_t* n_out) {
+  if (!types_out || !times_out || !n_out) return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    std::vector<uint32_t> t;
+    std::vector<int64_t> tm;
+    epi::generate_stream(neurons, duration_s, base_rate_hz, seed, embedded, rates, t, tm);
+    const size_t n = t.size();
+    auto* a = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (n ? n : 1)));
+    auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n ? n : 1)));
+    if (!a || !b) {
+      std::free(a);
+      std::free(b);
+      throw std::bad_alloc();
+    }
+    std::memcpy(a, t.data(), n * sizeof(uint32_t));
+    std::memcpy(b, tm.data(), n * sizeof(int64_t));
+    *types_out = a;
+    *times_out = b;
+    *n_out = n;
+  });
+}
+
+void epi_free(void* p) { std::free(p); }
+
+epi_status epi_generate_candidates(epi_ctx* ctx, uint64_t level, const epi_episode_batch* frequent,
+                                   const int64_t* alpha_low, const int64_t* alpha_high,
+                                   uint64_t n_alpha, uint32_t alphabet_size,
+                                   epi_episode_batch* out) {
+  if (!out) return EPI_EINVAL;
+  // Host-only: usable without a device. Output storage lives in ctx, or in
+  // thread-local storage when ctx is NULL.
+  static thread_local CandStore tls;
+  CandStore& E = ctx ? ctx->cands : tls;
+  std::string& err = ctx ? ctx->engine.err : g_free_err;
+  return guarded(err, [&] {
+    if (level < 1) throw epi::Error(EPI_EINVAL, "generate_candidates: level must be >= 1");
+    epi::EpisodeSet freq;
+    freq.N = static_cast<uint32_t>(level > 1 ? level - 1 : 1);
+    const uint64_t nf = (level > 1 && frequent) ? frequent->n_episodes : 0;
+    for (uint64_t e = 0; e < nf; ++e) {
+      const uint32_t b0 = frequent->offsets[e], N = frequent->offsets[e + 1] - b0;
+      if (N != freq.N) throw epi::Error(EPI_EINVAL, "generate_candidates: frequent episodes must have level-1 nodes");
+      const uint64_t cb = b0 - e;
+      freq.types.insert(freq.types.end(), frequent->types + b0, frequent->types + b0 + N);
+      freq.lo.insert(freq.lo.end(), frequent->low + cb, frequent->low + cb + N - 1);
+      freq.hi.insert(freq.hi.end(), frequent->high + cb, frequent->high + cb + N - 1);
+    }
+    std::vector<std::pair<int64_t, int64_t>> alpha;
+    for (uint64_t i = 0; i < n_alpha; ++i) alpha.emplace_back(alpha_low[i], alpha_high[i]);
+    epi::EpisodeSet outset;
+    epi::generate_candidates(level, freq, alpha, alphabet_size, outset);
+    const size_t n = outset.size();
+    const uint32_t N = outset.N;
+    E.gc_off.resize(n + 1);
+    for (size_t i = 0; i <= n; ++i) E.gc_off[i] = static_cast<uint32_t>(i * N);
+    E.gc_types = std::move(outset.types);
+    E.gc_lo = std::move(outset.lo);
+    E.gc_hi = std::move(outset.hi);
+    out->n_episodes = n;
+    out->offsets = E.gc_off.data();
+    out->types = E.gc_types.data();
+    out->low = E.gc_lo.data();
+    out->high = E.gc_hi.data();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Shared device/host helpers for the episodic_b200 kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace epi {
+
+// Stream time is bit-sliced into 32 ms tiles: bit b of tile g <-> compressed
+// time 32*g + b.
+constexpr int kTileBits = 32;
+// Gaps between consecutive events longer than this are capped at it while
+// loading (time compression). Exact for every constraint with high < kGapCap:
+// a capped gap still exceeds every admissible inter-event gap.
+constexpr int64_t kGapCap = 64;
+// Largest supported constraint upper bound on the bit-sliced path (two words
+// of per-position history behind the current tile).
+constexpr int64_t kMaxHigh = 63;
+// Longest episode handled by the templated kernels.
+constexpr int kMaxNodes = 16;
+
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(4 /*EPI_ECUDA*/, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define EPI_CUDA(x) ::epi::cuda_check((x), #x)
+
+}  // namespace epi
+
+#ifdef __CUDACC__
+namespace epi::dev {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 1-D bulk copy global -> shared (TMA engine, SASS UBLKCP), completion
+// signalled on `bar` as transaction bytes. dst/src 16-byte aligned, bytes a
+// multiple of 16.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+}  // namespace epi::dev
+#endif

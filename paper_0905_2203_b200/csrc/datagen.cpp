@@ -1,0 +1,167 @@
+// Synthetic spike-train generator: a bit-exact restatement of generate()
+// (E/datagen.hpp:71-122) so the bench and the parity tests build the same
+// streams as the reference without linking it.
+//   * per neuron: Rng(splitmix64(seed ^ (0x42 + neuron))), exponential
+//     inter-spike gaps, times truncated to ms   (E/datagen.hpp:91-98)
+//   * per embedded episode: Rng(splitmix64(seed ^ (0xE1BEDDED + (e << 20)))),
+//     exponential start gaps, uniform gaps inside each constraint window
+//                                                (E/datagen.hpp:100-115)
+//   * events sorted by (time, type)            (E/datagen.hpp:117-119)
+// The reference sorts stably; entries that compare equal under (time, type)
+// are identical values, so any sort yields the same stream. Neurons are
+// generated in parallel (each owns its RNG) and the sort is a parallel
+// chunk-sort + merge, so 10M-event streams build in well under a second.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "../../include/episodic_b200.h"
+#include "common.cuh"
+
+namespace epi {
+namespace {
+
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : gen_(seed) {}
+  double uniform01() { return (static_cast<double>(gen_() >> 11) + 1.0) * 0x1.0p-53; }
+  double exponential(double rate) { return -std::log(uniform01()) / rate; }
+  int64_t uniform_gap(int64_t lo, int64_t hi) {
+    return lo + 1 + static_cast<int64_t>(gen_() % static_cast<uint64_t>(hi - lo));
+  }
+
+ private:
+  std::mt19937_64 gen_;
+};
+
+struct Ev {
+  int64_t time;
+  uint32_t type;
+  bool operator<(const Ev& o) const { return time != o.time ? time < o.time : type < o.type; }
+};
+
+unsigned workers() {
+  unsigned hw = std::thread::hardware_concurrency();
+  return hw ? std::min(hw, 64u) : 1u;
+}
+
+template <class F>
+void parallel_for(size_t n, F&& f) {
+  unsigned w = std::min<size_t>(workers(), n ? n : 1);
+  std::vector<std::thread> th;
+  for (unsigned i = 1; i < w; ++i) th.emplace_back([&, i] {
+    for (size_t j = i; j < n; j += w) f(j);
+  });
+  for (size_t j = 0; j < n; j += w) f(j);
+  for (auto& t : th) t.join();
+}
+
+void parallel_sort(std::vector<Ev>& v) {
+  const size_t n = v.size();
+  unsigned w = workers();
+  if (n < (1u << 16) || w == 1) {
+    std::sort(v.begin(), v.end());
+    return;
+  }
+  size_t parts = 1;
+  while (parts * 2 <= w) parts *= 2;
+  std::vector<size_t> b(parts + 1);
+  for (size_t i = 0; i <= parts; ++i) b[i] = n * i / parts;
+  parallel_for(parts, [&](size_t i) { std::sort(v.begin() + b[i], v.begin() + b[i + 1]); });
+  std::vector<Ev> tmp(n);
+  std::vector<Ev>* src = &v;
+  std::vector<Ev>* dst = &tmp;
+  for (size_t width = 1; width < parts; width *= 2) {
+    const size_t pairs = parts / (2 * width);
+    parallel_for(pairs, [&](size_t p) {
+      size_t lo = b[2 * width * p], mid = b[2 * width * p + width], hi = b[2 * width * (p + 1)];
+      std::merge(src->begin() + lo, src->begin() + mid, src->begin() + mid, src->begin() + hi,
+                 dst->begin() + lo);
+    });
+    std::swap(src, dst);
+  }
+  if (src != &v) v.swap(*src);
+}
+
+}  // namespace
+
+// Returns the generated stream; throws Error(EPI_EINVAL) with the
+// reference's messages (E/datagen.hpp:72-80).
+void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                     const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
+                     std::vector<int64_t>& times) {
+  if (neurons < 1) throw Error(EPI_EINVAL, "generate: need at least one neuron");
+  if (duration_s < 0) throw Error(EPI_EINVAL, "generate: negative duration");
+  if (!(base_rate_hz > 0)) throw Error(EPI_EINVAL, "generate: base rate must be > 0");
+  const uint64_t ne = emb ? emb->n_episodes : 0;
+  for (uint64_t e = 0; e < ne; ++e) {
+    uint32_t b0 = emb->offsets[e], N = emb->offsets[e + 1] - b0;
+    if (N == 0) throw Error(EPI_EINVAL, "episode must have at least one node");
+    uint64_t cb = b0 - e;
+    for (uint32_t k = 0; k + 1 < N; ++k)
+      if (emb->low[cb + k] < 0 || emb->low[cb + k] >= emb->high[cb + k])
+        throw Error(EPI_EINVAL, "interval constraint requires 0 <= low < high");
+    if (!(rates[e] > 0)) throw Error(EPI_EINVAL, "generate: injection rate must be > 0");
+    for (uint32_t k = 0; k < N; ++k)
+      if (emb->types[b0 + k] >= neurons)
+        throw Error(EPI_EINVAL, "generate: embedded episode references unknown neuron");
+  }
+
+  std::vector<std::vector<Ev>> per(neurons + ne);
+  parallel_for(neurons + ne, [&](size_t j) {
+    std::vector<Ev>& out = per[j];
+    if (j < neurons) {
+      const uint32_t neuron = static_cast<uint32_t>(j);
+      Rng rng(splitmix64(seed ^ (0x42ULL + neuron)));
+      out.reserve(static_cast<size_t>(duration_s * base_rate_hz * 1.05) + 16);
+      double t = rng.exponential(base_rate_hz);
+      while (t < duration_s) {
+        out.push_back({static_cast<int64_t>(t * 1000.0), neuron});
+        t += rng.exponential(base_rate_hz);
+      }
+    } else {
+      const uint64_t e = j - neurons;
+      const uint32_t b0 = emb->offsets[e], N = emb->offsets[e + 1] - b0;
+      const uint64_t cb = b0 - e;
+      Rng rng(splitmix64(seed ^ (0xE1BEDDEDULL + (e << 20))));
+      double start_s = rng.exponential(rates[e]);
+      while (start_s < duration_s) {
+        int64_t t = static_cast<int64_t>(start_s * 1000.0);
+        out.push_back({t, emb->types[b0]});
+        for (uint32_t k = 1; k < N; ++k) {
+          t += rng.uniform_gap(emb->low[cb + k - 1], emb->high[cb + k - 1]);
+          out.push_back({t, emb->types[b0 + k]});
+        }
+        start_s += rng.exponential(rates[e]);
+      }
+    }
+  });
+  size_t total = 0;
+  for (auto& v : per) total += v.size();
+  std::vector<Ev> all;
+  all.reserve(total);
+  for (auto& v : per) {
+    all.insert(all.end(), v.begin(), v.end());
+    std::vector<Ev>().swap(v);
+  }
+  parallel_sort(all);
+  types.resize(total);
+  times.resize(total);
+  for (size_t i = 0; i < total; ++i) {
+    types[i] = all[i].type;
+    times[i] = all[i].time;
+  }
+}
+
+}  // namespace epi

@@ -1,0 +1,65 @@
+// Device-resident stream and scratch buffers owned by an epi_ctx.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace epi {
+
+// Growable device buffers addressed by slot; contents are not preserved
+// across growth.
+class DeviceScratch {
+ public:
+  ~DeviceScratch() {
+    for (auto& b : bufs_)
+      if (b.p) cudaFree(b.p);
+  }
+  template <class T>
+  T* get(size_t slot, size_t count) {
+    if (slot >= bufs_.size()) bufs_.resize(slot + 1);
+    Buf& b = bufs_[slot];
+    size_t bytes = count * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    if (bytes > b.bytes) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      size_t grow = bytes + bytes / 4;
+      EPI_CUDA(cudaMalloc(&b.p, grow));
+      b.bytes = grow;
+    }
+    return static_cast<T*>(b.p);
+  }
+
+ private:
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::vector<Buf> bufs_;
+};
+
+struct DeviceStream {
+  uint64_t n = 0;          // events
+  uint32_t alphabet = 0;   // event-type alphabet size
+  uint32_t a_pad = 4;      // words per tile row (alphabet rounded up to 4)
+  uint64_t n_tiles = 0;    // 32 ms tiles covering the compressed span
+  uint64_t span = 0;       // compressed time span (last compressed time + 1)
+  uint32_t* d_occ = nullptr;
+  size_t occ_bytes = 0;
+  uint64_t launches = 0;   // kernels launched by loads (stats)
+  std::vector<uint64_t> type_hist;  // events per type (a_pad entries; matched-pair model)
+
+  ~DeviceStream() { release(); }
+  void release();
+  void load(const uint32_t* d_types, const int64_t* d_times, uint64_t n_events, uint32_t alphabet,
+            cudaStream_t st, DeviceScratch& scratch);
+
+ private:
+  void ensure_occ(uint64_t tiles, cudaStream_t st);
+};
+
+}  // namespace epi

@@ -1,0 +1,97 @@
+// Host engine behind the C-ABI: owns the device stream, runs the two-pass
+// count and the level-wise miner. Host C++17; CUDA runtime only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/episodic_b200.h"
+#include "device_stream.h"
+
+namespace epi {
+
+// Flat list of episodes of one length N (the form every mining level has).
+struct EpisodeSet {
+  uint32_t N = 0;
+  std::vector<uint32_t> types;  // n * N
+  std::vector<int64_t> lo, hi;  // n * (N-1)
+  size_t size() const { return N ? types.size() / N : 0; }
+  void clear() {
+    types.clear();
+    lo.clear();
+    hi.clear();
+  }
+};
+
+struct PinnedBuffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuffer() {
+    if (p) cudaFreeHost(p);
+  }
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      size_t grow = need + need / 4 + 4096;
+      EPI_CUDA(cudaMallocHost(&p, grow));
+      bytes = grow;
+    }
+    return p;
+  }
+};
+
+class Engine {
+ public:
+  explicit Engine(int device);
+  ~Engine();
+
+  void load_stream_host(const uint32_t* types, const int64_t* times, uint64_t n, uint32_t alphabet);
+  void load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,
+                          uint32_t alphabet);
+  uint64_t stream_size() const { return stream_.n; }
+  uint64_t last_load_h2d = 0;
+  uint32_t alphabet() const { return stream_.alphabet; }
+
+  // Exact or two-pass count of one fixed-length set; counts[i] for set[i].
+  void count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
+                 std::vector<uint64_t>& counts, epi_stats& stats);
+  // Arbitrary CSR batch (mixed lengths): validated, grouped by length.
+  void count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
+                   uint64_t* counts_out, uint8_t* frequent_out, epi_stats* stats);
+  void mine(const epi_mine_config& cfg, epi_mine_result* out);
+
+  std::string err;
+  std::mutex mu;
+
+ private:
+  // Exact count of one fixed-length set on the device.
+  void count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
+                   double* ms_out);
+  void h2d(void* dst, const void* src, size_t bytes);
+
+  int device_;
+  int num_sms_ = 148;
+  cudaStream_t st_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, ev2_ = nullptr;
+  DeviceStream stream_;
+  DeviceScratch scratch_;
+  PinnedBuffer pin_up_, pin_down_;
+
+  // epi_mine result storage
+  std::vector<uint64_t> m_level_cands_, m_level_off_, m_counts_;
+  std::vector<double> m_level_ms_;
+  std::vector<uint32_t> m_off_, m_types_;
+  std::vector<int64_t> m_lo_, m_hi_;
+};
+
+// Apriori join, generate_candidates (E/miner.hpp:76-109).
+void generate_candidates(size_t level, const EpisodeSet& frequent,
+                         const std::vector<std::pair<int64_t, int64_t>>& alphabet,
+                         uint32_t alphabet_size, EpisodeSet& out);
+
+}  // namespace epi

@@ -1,0 +1,213 @@
+"""Parity of the B200 counting path (through the C-ABI) against the reference:
+golden known-answer tests, the reference's randomised corpora, the bench
+configs, and the oracle port on larger random instances. Bit-exact (integer
+counts), no tolerance."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from helpers import csr_of, ep_from_json, stream_from_json, fnv_u64s
+from instances import corpus
+from paper_0905_2203_b200 import (COUNT_PRUNED, MODE_EXACT, MODE_MINE, DataError, Embedding, Episode,
+                                  GenConfig, InvalidArgument, Unsupported, generate_arrays)
+
+pytestmark = pytest.mark.gpu
+
+BINS = [(0, 5), (5, 10), (10, 15)]
+
+
+def count_one(ctx, types, times, alphabet, eps, **kw):
+    ctx.load_arrays(np.asarray(types, np.uint32), np.asarray(times, np.int64), alphabet)
+    return ctx.count_csr(csr_of(eps), **kw)
+
+
+@pytest.fixture
+def segments_env():
+    old = os.environ.get("EPI_FORCE_SEGMENTS")
+
+    def set_(v):
+        if v is None:
+            os.environ.pop("EPI_FORCE_SEGMENTS", None)
+        else:
+            os.environ["EPI_FORCE_SEGMENTS"] = str(v)
+    yield set_
+    set_(old)
+
+
+def test_known_answer_tests(ctx, golden_kats):
+    for k in golden_kats["count"]:
+        types, times, a = stream_from_json(k)
+        got = count_one(ctx, types, times, a, [ep_from_json(k["episode"])])
+        assert int(got[0]) == k["expected"] == k["count_fsm"], k["name"]
+
+
+def test_known_answer_tests_many_segments(ctx, golden_kats, segments_env):
+    for p in (2, 3, 7, 64):
+        segments_env(p)
+        for k in golden_kats["count"]:
+            types, times, a = stream_from_json(k)
+            got = count_one(ctx, types, times, a, [ep_from_json(k["episode"])])
+            assert int(got[0]) == k["expected"], (k["name"], p)
+
+
+@pytest.mark.parametrize("force", [None, 2, 5, 13])
+def test_reference_corpora(ctx, golden_instances, segments_env, force):
+    """T/test_fsm.cpp, T/test_tracking.cpp, T/test_mapconcat.cpp,
+    T/acceptance.cpp C1 corpora: device count == reference count_fsm ==
+    oracle_count, at several forced segment counts (MapConcatenate
+    P-independence, cf. T/test_mapconcat.cpp:137-145)."""
+    segments_env(force)
+    for c in golden_instances:
+        gen = corpus(c["seed"], c["count"], c["max_events"], c["max_alphabet"], c["max_gap"],
+                     c["max_size"])
+        for i, ((types, times, a, et, cons), want) in enumerate(zip(gen, c["instances"])):
+            got = count_one(ctx, types, times, a, [(et, cons)])
+            assert int(got[0]) == want["count"], (c["name"], i, force)
+
+
+def _random_case(rng, n_max, alphabet_max, gap_max, n_nodes_max, high_max):
+    n = int(rng.integers(0, n_max + 1))
+    a = int(rng.integers(1, alphabet_max + 1))
+    times = np.cumsum(rng.integers(0, gap_max + 1, size=n)).astype(np.int64)
+    types = rng.integers(0, a, size=n).astype(np.uint32)
+    eps = []
+    for _ in range(int(rng.integers(1, 40))):
+        N = int(rng.integers(1, n_nodes_max + 1))
+        et = [int(x) for x in rng.integers(0, a, size=N)]
+        cons = []
+        for _k in range(N - 1):
+            hi = int(rng.integers(1, high_max + 1))
+            lo = int(rng.integers(0, hi))
+            cons.append((lo, hi))
+        eps.append((et, cons))
+    return types, times, a, eps
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_vs_port(ctx, seed, segments_env):
+    """Wider random instances than the reference's (windows up to 63, up to
+    10 nodes, thousands of events, idle gaps that trigger time compression)
+    against the oracle port (count_fsm restated)."""
+    rng = np.random.default_rng(1000 + seed)
+    for it in range(60):
+        segments_env([None, 3, 11][it % 3])
+        gap_max = [3, 12, 90][it % 3]
+        types, times, a, eps = _random_case(rng, 3000, 8, gap_max, 10, 63)
+        got = count_one(ctx, types, times, a, eps)
+        csr = csr_of(eps)
+        want = oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=4)
+        np.testing.assert_array_equal(got, want, err_msg=f"seed {seed} it {it}")
+
+
+def test_edge_cases(ctx):
+    # empty stream
+    assert list(count_one(ctx, [], [], 3, [([0, 1], [(0, 5)]), ([2], [])])) == [0, 0]
+    # every event at one timestamp: nothing chains; singletons collapse
+    got = count_one(ctx, [0, 1, 0, 1], [7, 7, 7, 7], 2, [([0, 1], [(0, 5)]), ([0], []), ([1], [])])
+    assert list(got) == [0, 1, 1]
+    # types outside the alphabet never fire (count_fsm returns 0)
+    got = count_one(ctx, [0, 1], [0, 7], 2, [([0, 5], [(5, 10)]), ([9], [])])
+    assert list(got) == [0, 0]
+    # high = 63 exactly at the edge, across a tile boundary
+    got = count_one(ctx, [0, 1, 0, 1], [0, 63, 70, 134], 2, [([0, 1], [(0, 63)]), ([0, 1], [(62, 63)])])
+    assert list(got) == [1, 1]
+    # 16-node episode with repeated types
+    ev_t = [i % 3 for i in range(400)]
+    ev_tm = list(range(0, 1200, 3))
+    ep = ([0, 1, 2] * 5 + [0], [(0, 5)] * 15)
+    got = count_one(ctx, ev_t, ev_tm, 3, [ep])
+    assert int(got[0]) == oracle.count_fsm(ev_t, ev_tm, ep[0], [c[0] for c in ep[1]], [c[1] for c in ep[1]])
+    # long idle gaps (compression) and times far from zero
+    t0 = 10**12
+    got = count_one(ctx, [0, 1, 0, 1], [t0, t0 + 7, t0 + 10**9, t0 + 10**9 + 6], 2, [([0, 1], [(5, 10)])])
+    assert int(got[0]) == 2
+
+
+def test_errors(ctx):
+    with pytest.raises(DataError, match="non-decreasing"):
+        ctx.load_arrays(np.array([0, 0], np.uint32), np.array([5, 4], np.int64), 1)
+    with pytest.raises(DataError, match="negative event time"):
+        ctx.load_arrays(np.array([0, 0], np.uint32), np.array([1, -4], np.int64), 1)
+    with pytest.raises(DataError, match="type id out of range"):
+        ctx.load_arrays(np.array([0, 3], np.uint32), np.array([1, 4], np.int64), 2)
+    # first offending event decides
+    with pytest.raises(DataError, match="type id out of range"):
+        ctx.load_arrays(np.array([5, 0, 0], np.uint32), np.array([1, 0, -1], np.int64), 2)
+    ctx.load_arrays(np.array([0, 1], np.uint32), np.array([0, 7], np.int64), 2)
+    with pytest.raises(InvalidArgument, match="0 <= low < high"):
+        ctx.count_csr(csr_of([([0, 1], [(5, 5)])]))
+    with pytest.raises(InvalidArgument, match="at least one node"):
+        ctx.count_csr(csr_of([([], [])]))
+    with pytest.raises(Unsupported):
+        ctx.count_csr(csr_of([([0, 1], [(5, 100)])]))
+
+
+def _gen(name):
+    if name == "cfg1":
+        return GenConfig(26, 60, 32, [Embedding(Episode([0, 1, 2, 3], [(5, 10)] * 3), 2.0)], 1)
+    if name == "cfg2":
+        eps = [([0, 1, 2, 3], [BINS[1]] * 3), ([4, 5, 6, 7], [BINS[0], BINS[1], BINS[2]]),
+               ([8, 9, 10, 11], [BINS[2], BINS[0], BINS[1]]), ([12, 13, 14, 15], [BINS[1], BINS[2], BINS[0]])]
+        return GenConfig(26, 60, 32, [Embedding(Episode(t, c), 5.0) for t, c in eps], 1)
+    if name == "cfg3":
+        return GenConfig(64, 7813, 20, [], 3)
+    raise KeyError(name)
+
+
+def test_cfg1_all_pairs(ctx, golden_configs):
+    g = golden_configs["cfg1"]
+    types, times = generate_arrays(_gen("cfg1"))
+    assert len(types) == g["n"]
+    ctx.load_arrays(types, times, 26)
+    eps = [([a, b], [(5, 10)]) for a in range(26) for b in range(26)]
+    got = ctx.count_csr(csr_of(eps))
+    assert [int(x) for x in got] == g["counts"]
+    assert int(got.sum()) == g["sum"] == 176437
+    assert fnv_u64s(got) == g["fnv_counts"]
+
+
+@pytest.mark.parametrize("mode", [MODE_MINE, MODE_EXACT])
+def test_cfg2_mining(ctx, golden_configs, mode):
+    from paper_0905_2203_b200 import MiningConfig, mine, write_mining_csv, EventStream
+    g = golden_configs["cfg2"]
+    types, times = generate_arrays(_gen("cfg2"))
+    s = EventStream(types, times, 26)
+    r = mine(s, MiningConfig(threshold=250, constraint_alphabet=BINS, max_level=4, mode=mode), ctx=ctx)
+    assert [lv.candidates for lv in r.levels] == g["level_candidates"] == [26, 2028, 142228, 4]
+    assert write_mining_csv(r) == g["csv"]
+    if mode == MODE_MINE:
+        assert r.stats["pruned"] > 0
+
+
+def test_cfg2_level3_bounds_sound(ctx, golden_configs):
+    """Pass 1 never prunes a frequent candidate, and its bound is >= exact."""
+    from paper_0905_2203_b200 import generate_candidates, Episode as E
+    types, times = generate_arrays(_gen("cfg2"))
+    ctx.load_arrays(types, times, 26)
+    l1 = [E([t], []) for t in range(26)]
+    l2 = generate_candidates(2, l1, BINS, 26)
+    c2 = ctx.count_csr(csr_of([(e.types, e.constraints) for e in l2]))
+    f2 = [e for e, c in zip(l2, c2) if c >= 250]
+    l3 = generate_candidates(3, f2, BINS, 26)
+    assert len(l3) == 142228
+    csr3 = csr_of([(e.types, e.constraints) for e in l3])
+    exact = ctx.count_csr(csr3, threshold=250, mode=MODE_EXACT)
+    mined, freq = ctx.count_csr(csr3, threshold=250, mode=MODE_MINE, with_frequent=True)
+    keep = mined != np.uint64(COUNT_PRUNED)
+    np.testing.assert_array_equal(mined[keep], exact[keep])
+    assert np.all(exact[~keep] < 250)
+    np.testing.assert_array_equal(freq.astype(bool), exact >= 250)
+    assert int((exact >= 250).sum()) == 8
+
+
+def test_cfg3_first_candidates(ctx, golden_configs):
+    g = golden_configs["cfg3"]
+    types, times = generate_arrays(_gen("cfg3"))
+    assert len(types) == g["n"] == 10004428
+    ctx.load_arrays(types, times, 64)
+    eps = [ep_from_json(e) for e in g["episodes"]]
+    got = ctx.count_csr(csr_of(eps))
+    assert [int(x) for x in got] == g["counts"]
+    assert int(got[:64].sum()) == g["sum_first64"] == 87180
