@@ -19,6 +19,8 @@ constexpr int64_t kGapCap = 64;
 // Largest supported constraint upper bound on the bit-sliced path (two words
 // of per-position history behind the current tile).
 constexpr int64_t kMaxHigh = 63;
+// Largest constraint upper bound on the wide path (128-word history ring).
+constexpr int64_t kMaxHighWide = 4095;
 // Longest episode handled by the templated kernels.
 constexpr int kMaxNodes = 16;
 

@@ -17,9 +17,10 @@ struct CountLaunch {
   int32_t P;               // segments
   int32_t window_tiles;    // tiles staged before a segment for its window
   int32_t chunk_tiles;     // tiles per shared-memory stage
+  int32_t hist_words;      // wide path: history words per position (ceil(max high / 32))
   uint32_t n_eps;          // episodes (all of length n_nodes)
   const uint32_t* ep_types;  // [n_eps * N]
-  const uint32_t* ep_win;    // [n_eps * (N-1)]: (low+1) | high << 8
+  const uint32_t* ep_win;    // [n_eps * (N-1)]: (low+1) | high << 16
   const uint32_t* ep_sigma;  // [n_eps]: sum of highs
   uint32_t* f_count;         // [P * n_eps] FRESH completions inside the segment
   uint32_t* f_ncomp;         // [P * n_eps] FRESH completions incl. window
@@ -30,7 +31,11 @@ struct CountLaunch {
 };
 
 uint32_t chunk_tiles_for(uint32_t a_pad);
-void launch_machines(int n_nodes, const CountLaunch& p, cudaStream_t st);
+// width: launch-uniform window width high-low (0 = mixed) selects a specialised kernel.
+void launch_machines(int n_nodes, int width, const CountLaunch& p, cudaStream_t st);
 void launch_walk(int n_nodes, const CountLaunch& p, cudaStream_t st);
+// high > 63 (up to kMaxHighWide): local-memory history ring.
+void launch_machines_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
+void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 
 }  // namespace epi

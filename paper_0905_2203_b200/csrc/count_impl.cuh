@@ -1,0 +1,566 @@
+// Exact non-overlapped episode counting on sm_100a: a bit-sliced counting
+// automaton, run segment-parallel (MapConcatenate) and stitched by a
+// per-episode concat walk. Included by count.cu (narrow windows, high <= 63)
+// and count_wide.cu (high <= 4095); see DESIGN.md.
+//
+// Semantics follow run_fsm / count_fsm (E/fsm.hpp:45-106) exactly:
+//   * an event of type tau at time t is admitted at position 0 iff t > pe
+//     (pe = time of the last counted completion, E/fsm.hpp:66-68);
+//   * at position k >= 1 iff some entry of position k-1 has time in
+//     [t-high, t-low)  (E/fsm.hpp:73-79);
+//   * admitting the last position counts one occurrence, sets pe = t and
+//     clears every list (E/fsm.hpp:83-91).
+// Because every admissible gap is >= 1 (low >= 0), admissions at time t only
+// read entries older than t. So the automaton's behaviour depends only on the
+// set of distinct firing times per type, the order of tied events does not
+// matter, and a whole 32 ms tile can be advanced with word-wide bit
+// operations:
+//
+//   C_0 = occ(tau_0) & (times > pe)
+//   C_k = occ(tau_k) & OR_{a=low+1..high} (C_{k-1} : history_{k-1}) << a
+//
+// where history_{k-1} holds the entry bitmaps of the previous tiles. The
+// first set bit of C_{N-1} is a completion; the tile is then recomputed above
+// it with empty history (the reference's list clear). Rare, so the loop is
+// off the hot path.
+//
+// MapConcatenate (E/mapconcat.hpp:71-159, paper PAPER.md:249-266): the tile
+// range is cut into P segments. The automaton state at a segment start T is
+// either FRESH (the last completion is older than T - sum(high): no live
+// entry can predate the window [T - sum(high), T), so a machine started empty
+// at the window start reaches the true state) or RESTART(L) (the last
+// completion L lies inside the window: the state is "cleared at L, pe = L").
+// The map kernel runs the FRESH machine of every (episode, segment) in
+// parallel and records its count, last completion and first kRecorded
+// completion times. The concat walk (one thread per episode) chains the
+// segments; when a boundary needs RESTART(L) it re-runs that machine inline
+// only until it completes at a time where the FRESH machine also completed -
+// from there both are identical, so the rest of the segment is read off the
+// FRESH record ("patch", cf. E/mapconcat.hpp:144-148).
+#pragma once
+
+#include "common.cuh"
+#include "count.h"
+
+namespace epi {
+namespace impl {
+
+constexpr int kMachThreads = 256;
+constexpr int kStages = 3;
+constexpr uint32_t kStageBytes = 8192;
+
+template <int N>
+struct EpParams {
+  static constexpr int M = N > 1 ? N - 1 : 1;
+  uint32_t type[N];
+  uint32_t lo1[M];  // low + 1
+  uint32_t hi[M];   // high
+  uint32_t sigma;   // sum of highs (MapConcatenate window)
+};
+
+template <int N>
+__device__ __forceinline__ EpParams<N> load_episode(const CountLaunch& p, uint32_t e) {
+  EpParams<N> ep;
+#pragma unroll
+  for (int k = 0; k < N; ++k) ep.type[k] = p.ep_types[static_cast<size_t>(e) * N + k];
+#pragma unroll
+  for (int k = 0; k < EpParams<N>::M; ++k) {
+    uint32_t w = N > 1 ? p.ep_win[static_cast<size_t>(e) * (N - 1) + k] : 0x10001u;
+    ep.lo1[k] = w & 0xffff;
+    ep.hi[k] = w >> 16;
+  }
+  ep.sigma = p.ep_sigma[e];
+  return ep;
+}
+
+// ---- history policies -------------------------------------------------------
+
+// Window test over X = (c : h1 : h2) (96 bits, c the current tile): bit i of
+// the result is set iff X has a set bit at age a in [lo1, hi] from time
+// 32*g + i, i.e. at X index 64 + i - a. With Z = X >> (64 - hi) (64 bits,
+// Z[j] = X[64 - hi + j]) this is OR_{b < w} Z[i + b], w = hi - lo1 + 1:
+// two funnel shifts to extract Z, then a smear of width w. Branch-free;
+// requires w <= 32 (wider windows are split in two).
+template <int W>
+__device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
+                                               uint32_t hi) {
+  const uint32_t s = 64u - hi;  // 1..63
+  const bool low = s < 32u;
+  const uint32_t w0 = low ? h2 : h1;
+  const uint32_t w1 = low ? h1 : c;
+  const uint32_t w2 = low ? c : 0u;
+  const uint32_t zl = __funnelshift_r(w0, w1, s & 31u);
+  const uint32_t zh = __funnelshift_r(w1, w2, s & 31u);
+  if constexpr (W > 0) {
+    uint32_t d = zl;
+#pragma unroll
+    for (int b = 1; b < W; ++b) d |= __funnelshift_r(zl, zh, b);
+    return d;
+  } else {
+    // runtime width: doubling smear, cover 1 -> 2 -> 4 -> ... -> w
+    const uint32_t w = hi - lo1 + 1u;
+    uint32_t rl = zl, rh = zh, cover = 1;
+#pragma unroll
+    for (int step = 0; step < 5; ++step) {
+      const uint32_t sh = cover < w ? (cover < w - cover ? cover : w - cover) : 0u;
+      rl |= __funnelshift_r(rl, rh, sh);
+      rh |= rh >> sh;
+      cover += sh;
+    }
+    return rl;
+  }
+}
+
+// high <= 63: the entry bitmaps of the two previous tiles, in registers.
+// W > 0: every window of the launch has width high - low == W (compile-time
+// unrolled smear); W == 0: runtime widths.
+template <int N, int W = 0>
+struct NarrowHist {
+  static constexpr int M = N > 1 ? N - 1 : 1;
+  uint32_t h1[M];
+  uint32_t h2[M];
+
+  __device__ __forceinline__ void reset(int32_t, int) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) h1[k] = h2[k] = 0;
+  }
+  __device__ __forceinline__ void on_clear(int32_t) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) h1[k] = h2[k] = 0;
+  }
+  __device__ __forceinline__ static uint32_t dil(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
+                                                 uint32_t hi) {
+    if constexpr (W > 0) {
+      return window_any<W>(c, h1, h2, lo1, hi);
+    } else {
+      if (hi - lo1 < 32u) return window_any<0>(c, h1, h2, lo1, hi);
+      return window_any<0>(c, h1, h2, lo1, lo1 + 31u) | window_any<0>(c, h1, h2, lo1 + 32u, hi);
+    }
+  }
+  __device__ __forceinline__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi,
+                                             int32_t) const {
+    return dil(c, h1[k], h2[k], lo1, hi);
+  }
+  __device__ __forceinline__ static uint32_t dilate_fresh(uint32_t c, uint32_t lo1, uint32_t hi) {
+    return dil(c, 0u, 0u, lo1, hi);
+  }
+  __device__ __forceinline__ void push(const uint32_t* C, int32_t) {
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) {
+      h2[k] = h1[k];
+      h1[k] = C[k];
+    }
+  }
+};
+
+// high <= 32*HWMAX: a ring of per-tile entry bitmaps in local memory, `hw`
+// words deep (uniform per launch). Tiles older than `clear_tile` read as 0,
+// so a clear costs O(1).
+template <int N, int HWMAX>
+struct WideHist {
+  static constexpr int M = N > 1 ? N - 1 : 1;
+  static constexpr int kMask = HWMAX - 1;
+  uint32_t ring[M][HWMAX];
+  int head;          // slot of the newest pushed tile word
+  int32_t last;      // tile index of the newest pushed word
+  int32_t clear_tile;
+  int hw;
+
+  __device__ __forceinline__ void reset(int32_t g_start, int hw_) {
+    head = 0;
+    last = g_start - 1;
+    clear_tile = g_start;
+    hw = hw_;
+  }
+  __device__ __forceinline__ void on_clear(int32_t g) { clear_tile = g; }
+
+  // Word widx in [0, hw] of X = (hw history words, then the current tile):
+  // widx == hw is `c`, widx == hw - j is the tile j back.
+  __device__ __forceinline__ uint32_t word(int k, int widx, uint32_t c, int32_t g) const {
+    if (widx >= hw) return widx == hw ? c : 0u;
+    const int j = hw - widx;
+    const int32_t tile = g - j;
+    if (tile < clear_tile || tile > last) return 0u;
+    return ring[k][(head - (last - tile)) & kMask];
+  }
+  __device__ __forceinline__ uint32_t slice32(int k, int x, uint32_t c, int32_t g) const {
+    const int w = x >> 5, s = x & 31;
+    return __funnelshift_r(word(k, w, c, g), word(k, w + 1, c, g), s);
+  }
+  __device__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi, int32_t g) const {
+    const int A = static_cast<int>(lo1), B = static_cast<int>(hi);
+    const int P0 = 32 * hw - B, P1 = 32 * hw - A;
+    const int w = B - A + 1;  // window width (high - low)
+    if (w <= 32) {
+      uint64_t r = static_cast<uint64_t>(slice32(k, P0, c, g)) |
+                   (static_cast<uint64_t>(slice32(k, P0 + 32, c, g)) << 32);
+      int cover = 1;
+      while (cover < w) {
+        const int sh = cover < w - cover ? cover : w - cover;
+        r |= r >> sh;
+        cover += sh;
+      }
+      return static_cast<uint32_t>(r);
+    }
+    // interior [P0+31, P1] is inside every bit's window
+    bool any = false;
+    const int lo = P0 + 31, hix = P1;
+    for (int wi = lo >> 5; wi <= (hix >> 5) && !any; ++wi) {
+      uint32_t m = ~0u;
+      if (wi == (lo >> 5)) m &= ~0u << (lo & 31);
+      if (wi == (hix >> 5)) m &= (hix & 31) == 31 ? ~0u : ((1u << ((hix & 31) + 1)) - 1u);
+      any = (word(k, wi, c, g) & m) != 0;
+    }
+    uint32_t sl = slice32(k, P0, c, g) & 0x7fffffffu;  // left edge: any(X[P0+i .. P0+30])
+    sl |= sl >> 1;
+    sl |= sl >> 2;
+    sl |= sl >> 4;
+    sl |= sl >> 8;
+    sl |= sl >> 16;
+    uint32_t sr = (slice32(k, P1 + 1, c, g) & 0x7fffffffu) << 1;  // right: any(X[P1+1 .. P1+i])
+    sr |= sr << 1;
+    sr |= sr << 2;
+    sr |= sr << 4;
+    sr |= sr << 8;
+    sr |= sr << 16;
+    return (any ? ~0u : 0u) | sl | sr;
+  }
+  __device__ __forceinline__ static uint32_t dilate_fresh(uint32_t c, uint32_t lo1, uint32_t hi) {
+    uint32_t d = 0;
+    const uint32_t e1 = hi < 31u ? hi : 31u;
+    for (uint32_t a = lo1; a <= e1; ++a) d |= c << a;
+    return d;
+  }
+  __device__ __forceinline__ void push(const uint32_t* C, int32_t g) {
+    head = (head + 1) & kMask;
+    last = g;
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) ring[k][head] = C[k];
+  }
+};
+
+template <int N, class Hist>
+struct Machine {
+  Hist hist;
+  int32_t thr_tile;   // position 0 admits only times > thr:
+  uint32_t thr_mask;  // tiles < thr_tile none, tile == thr_tile thr_mask
+
+  __device__ __forceinline__ void set_threshold(int64_t thr) {
+    if (thr < 0) {
+      thr_tile = -1;
+      thr_mask = ~0u;
+    } else {
+      thr_tile = static_cast<int32_t>(thr >> 5);
+      uint32_t b = static_cast<uint32_t>(thr & 31);
+      thr_mask = b == 31 ? 0u : (~0u << (b + 1));
+    }
+  }
+};
+
+// Advance one tile. on_completion(time) returns true to stop the machine.
+template <int N, class Hist, class OnC>
+__device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>& ep,
+                                          const uint32_t (&occ)[N], int32_t g, OnC&& on_c) {
+  uint32_t C[N];
+  C[0] = occ[0];
+  if (g <= m.thr_tile) C[0] &= (g < m.thr_tile) ? 0u : m.thr_mask;
+#pragma unroll
+  for (int k = 1; k < N; ++k)
+    C[k] = occ[k] & m.hist.dilate(k - 1, C[k - 1], ep.lo1[k - 1], ep.hi[k - 1], g);
+  if (C[N - 1]) {
+    uint32_t last = C[N - 1];
+    do {
+      const int b = __ffs(last) - 1;
+      const uint64_t tc = static_cast<uint64_t>(g) * 32 + b;
+      if (on_c(tc)) return true;
+      const uint32_t msk = b == 31 ? 0u : (~0u << (b + 1));
+      m.thr_tile = g;
+      m.thr_mask = msk;
+      C[0] = occ[0] & msk;
+#pragma unroll
+      for (int k = 1; k < N; ++k) C[k] = occ[k] & Hist::dilate_fresh(C[k - 1], ep.lo1[k - 1], ep.hi[k - 1]);
+      last = C[N - 1];
+    } while (last);
+    m.hist.on_clear(g);  // the clear also empties older history
+  }
+  m.hist.push(C, g);
+  return false;
+}
+
+// Map step: FRESH machine of (episode, segment). Tiles of the segment (plus
+// its window) are staged through shared memory with bulk copies; every
+// thread of the CTA walks the same tiles, so one staged row serves all 256
+// episodes of the block.
+template <int N, class Hist>
+__global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunch p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem + 128);
+  const uint32_t a_pad = p.a_pad;
+  const uint32_t ch = static_cast<uint32_t>(p.chunk_tiles);
+  const uint32_t stage_words = ch * a_pad;
+
+  const int q = blockIdx.y;
+  const uint32_t e = blockIdx.x * kMachThreads + threadIdx.x;
+  const bool active = e < p.n_eps;
+  const int32_t gq = p.seg_g[q];
+  const int32_t gend = p.seg_g[q + 1];
+  const int32_t g0 = gq - p.window_tiles > 0 ? gq - p.window_tiles : 0;
+
+  EpParams<N> ep = load_episode<N>(p, active ? e : 0);
+  Machine<N, Hist> m;
+  m.hist.reset(g0, p.hist_words);
+  const int64_t tq = static_cast<int64_t>(gq) * 32;
+  int64_t s0 = q == 0 ? 0 : tq - static_cast<int64_t>(ep.sigma);
+  if (s0 < 0) s0 = 0;
+  m.set_threshold(s0 - 1);
+
+  uint32_t cnt = 0, ncomp = 0;
+  uint64_t last = ~0ull;
+  uint64_t* first = p.f_first + (static_cast<size_t>(q) * p.n_eps + e) * kRecorded;
+
+  const int32_t total_tiles = gend - g0;
+  const int32_t nchunks = (total_tiles + static_cast<int32_t>(ch) - 1) / static_cast<int32_t>(ch);
+
+  auto issue = [&](int32_t c) {
+    const int32_t tg = g0 + c * static_cast<int32_t>(ch);
+    int32_t nt = gend - tg;
+    if (nt > static_cast<int32_t>(ch)) nt = static_cast<int32_t>(ch);
+    const uint32_t bytes = static_cast<uint32_t>(nt) * a_pad * 4u;
+    uint64_t* bar = &bars[c % kStages];
+    dev::fence_proxy_async();
+    dev::mbar_arrive_expect_tx(bar, bytes);
+    dev::bulk_g2s(stage + static_cast<size_t>(c % kStages) * stage_words,
+                  p.occ + static_cast<size_t>(tg) * a_pad, bytes, bar);
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) dev::mbar_init(&bars[s], 1);
+    dev::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int32_t c = 0; c < kStages - 1 && c < nchunks; ++c) issue(c);
+
+  auto on_c = [&](uint64_t tc) -> bool {
+    if (ncomp < kRecorded && active) first[ncomp] = tc;
+    ++ncomp;
+    if (static_cast<int64_t>(tc) >= tq) {
+      ++cnt;
+      last = tc;
+    }
+    return false;
+  };
+
+  for (int32_t c = 0; c < nchunks; ++c) {
+    if (threadIdx.x == 0 && c + kStages - 1 < nchunks) issue(c + kStages - 1);
+    dev::mbar_wait(&bars[c % kStages], static_cast<uint32_t>(c / kStages) & 1u);
+    const uint32_t* buf = stage + static_cast<size_t>(c % kStages) * stage_words;
+    const int32_t tg = g0 + c * static_cast<int32_t>(ch);
+    int32_t nt = gend - tg;
+    if (nt > static_cast<int32_t>(ch)) nt = static_cast<int32_t>(ch);
+    for (int32_t t = 0; t < nt; ++t) {
+      const uint32_t* row = buf + static_cast<size_t>(t) * a_pad;
+      uint32_t occ[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) occ[k] = row[ep.type[k]];
+      tile_step<N, Hist>(m, ep, occ, tg + t, on_c);
+    }
+    __syncthreads();
+  }
+
+  if (active) {
+    const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
+    p.f_count[idx] = cnt;
+    p.f_ncomp[idx] = ncomp;
+    p.f_last[idx] = last;
+  }
+}
+
+// Concat step: one thread per episode chains the P segment records.
+template <int N, class Hist>
+__global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.n_eps) return;
+  const EpParams<N> ep = load_episode<N>(p, e);
+  uint64_t total = 0;
+  bool restart = false;
+  uint64_t L = 0;
+  uint32_t patches = 0;
+  // Segment records do not depend on the walk state: fetch them kPrefetch
+  // segments at a time so the loads overlap instead of serialising.
+  constexpr int kPrefetch = 8;
+  uint32_t pf_cnt[kPrefetch];
+  uint64_t pf_last[kPrefetch];
+  for (int q = 0; q < p.P; ++q) {
+    if (q % kPrefetch == 0) {
+#pragma unroll
+      for (int j = 0; j < kPrefetch; ++j) {
+        const int qq = q + j;
+        const size_t ix = static_cast<size_t>(qq) * p.n_eps + e;
+        pf_cnt[j] = qq < p.P ? p.f_count[ix] : 0u;
+        pf_last[j] = qq < p.P ? p.f_last[ix] : ~0ull;
+      }
+    }
+    const int32_t gq = p.seg_g[q];
+    const int32_t gn = p.seg_g[q + 1];
+    const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
+    const uint32_t fcnt = pf_cnt[q % kPrefetch];
+    const uint64_t flast = pf_last[q % kPrefetch];
+    uint32_t cnt = fcnt;
+    uint64_t last = flast;
+    if (restart) {
+      ++patches;
+      const uint64_t tq = static_cast<uint64_t>(gq) * 32;
+      const uint32_t nf = p.f_ncomp[idx];
+      const uint32_t nrec = nf < kRecorded ? nf : kRecorded;
+      uint64_t first[kRecorded];
+#pragma unroll
+      for (int j = 0; j < kRecorded; ++j)
+        first[j] = j < static_cast<int>(nrec) ? p.f_first[idx * kRecorded + j] : ~0ull;
+      Machine<N, Hist> m;
+      const int32_t gL = static_cast<int32_t>(L >> 5);
+      m.hist.reset(gL, p.hist_words);
+      m.set_threshold(static_cast<int64_t>(L));
+      uint32_t rc = 0;
+      uint64_t rl = ~0ull;
+      bool synced = false;
+      // Quiet-window sync: once both machines' last clear (R: its restart or
+      // last completion; F: its fresh start at the window or its last
+      // completion) lies more than sum(high) before T, every live entry at T
+      // comes from chains starting in [T - sum(high), T), which both machines
+      // hold identically, and pe no longer matters: from T on, R == F.
+      const int64_t sigma = static_cast<int64_t>(ep.sigma);
+      const int64_t f_start = static_cast<int64_t>(tq) - sigma - 1;  // F admits starts >= window
+      int64_t last_r = static_cast<int64_t>(L);
+      auto quiet = [&](int64_t T) -> bool {
+        if (last_r + sigma >= T) return false;
+        if (nf > static_cast<uint32_t>(kRecorded) && static_cast<int64_t>(first[kRecorded - 1]) < T)
+          return false;  // F completions before T not all recorded
+        int64_t last_f = f_start;
+        uint32_t f_before = 0;  // F in-segment completions before T
+#pragma unroll
+        for (int j = 0; j < kRecorded; ++j)
+          if (j < static_cast<int>(nrec) && static_cast<int64_t>(first[j]) < T) {
+            last_f = static_cast<int64_t>(first[j]);
+            if (first[j] >= tq) ++f_before;
+          }
+        if (last_f + sigma >= T) return false;
+        const uint32_t rest = fcnt - f_before;
+        cnt = rc + rest;
+        last = rest ? flast : rl;
+        return true;
+      };
+      auto on_c = [&](uint64_t tc) -> bool {
+        if (tc >= tq) {
+          ++rc;
+          rl = tc;
+        }
+        last_r = static_cast<int64_t>(tc);
+        uint32_t inseg = 0;
+#pragma unroll
+        for (int j = 0; j < kRecorded; ++j) {
+          if (j < static_cast<int>(nrec)) {
+            if (first[j] >= tq) ++inseg;
+            if (first[j] == tc) {
+              const uint32_t rest = fcnt - inseg;
+              cnt = rc + rest;
+              last = rest ? flast : rl;
+              synced = true;
+              return true;
+            }
+          }
+        }
+        return false;
+      };
+      for (int32_t g = gL; g < gn; ++g) {
+        if (g > gL && quiet(static_cast<int64_t>(g) * 32)) {
+          synced = true;
+          break;
+        }
+        const uint32_t* row = p.occ + static_cast<size_t>(g) * p.a_pad;
+        uint32_t occ[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) occ[k] = __ldg(row + ep.type[k]);
+        if (tile_step<N, Hist>(m, ep, occ, g, on_c)) break;
+      }
+      if (!synced) {
+        cnt = rc;
+        last = rl;
+      }
+    }
+    total += cnt;
+    const int64_t wn = static_cast<int64_t>(gn) * 32 - static_cast<int64_t>(ep.sigma);
+    restart = (q + 1 < p.P) && cnt > 0 && static_cast<int64_t>(last) >= wn;
+    L = last;
+  }
+  p.counts[e] = total;
+  if (patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));
+}
+
+template <int N, class Hist>
+void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
+  const uint32_t stage_words = static_cast<uint32_t>(p.chunk_tiles) * p.a_pad;
+  const size_t smem = 128 + static_cast<size_t>(kStages) * stage_words * 4;
+  static bool configured = false;
+  if (!configured) {
+    EPI_CUDA(cudaFuncSetAttribute(machines_kernel<N, Hist>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured = true;
+  }
+  dim3 grid((p.n_eps + kMachThreads - 1) / kMachThreads, p.P);
+  machines_kernel<N, Hist><<<grid, kMachThreads, smem, st>>>(p);
+  EPI_CUDA(cudaGetLastError());
+}
+
+template <int N, class Hist>
+void launch_walk_n(const CountLaunch& p, cudaStream_t st) {
+  walk_kernel<N, Hist><<<(p.n_eps + 127) / 128, 128, 0, st>>>(p);
+  EPI_CUDA(cudaGetLastError());
+}
+
+// Runtime N -> template N dispatch for a history policy family H<N>.
+template <template <int> class H, int... Ns>
+struct Dispatch;
+
+template <template <int> class H>
+struct Dispatch<H> {
+  static void machines(int, const CountLaunch&, cudaStream_t) {
+    throw Error(7, "episode length not supported by the device counter");
+  }
+  static void walk(int, const CountLaunch&, cudaStream_t) {
+    throw Error(7, "episode length not supported by the device counter");
+  }
+};
+
+template <template <int> class H, int N, int... Rest>
+struct Dispatch<H, N, Rest...> {
+  static void machines(int n, const CountLaunch& p, cudaStream_t st) {
+    if (n == N)
+      launch_machines_n<N, H<N>>(p, st);
+    else
+      Dispatch<H, Rest...>::machines(n, p, st);
+  }
+  static void walk(int n, const CountLaunch& p, cudaStream_t st) {
+    if (n == N)
+      launch_walk_n<N, H<N>>(p, st);
+    else
+      Dispatch<H, Rest...>::walk(n, p, st);
+  }
+};
+
+template <int W>
+struct NarrowW {
+  template <int N>
+  using H = NarrowHist<N, W>;
+};
+
+// Uniform-window-width map kernels (N 2..8), instantiated per W in
+// count_w*.cu so the compile parallelises.
+template <int W>
+void launch_machines_w(int n, const CountLaunch& p, cudaStream_t st) {
+  Dispatch<NarrowW<W>::template H, 2, 3, 4, 5, 6, 7, 8>::machines(n, p, st);
+}
+
+}  // namespace impl
+}  // namespace epi

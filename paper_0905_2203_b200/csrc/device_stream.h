@@ -45,20 +45,28 @@ class DeviceScratch {
 struct DeviceStream {
   uint64_t n = 0;          // events
   uint32_t alphabet = 0;   // event-type alphabet size
-  uint32_t a_pad = 4;      // words per tile row (alphabet rounded up to 4)
+  uint32_t a_pad = 4;      // words per tile row (alphabet + 1 spare, rounded up to 4)
   uint64_t n_tiles = 0;    // 32 ms tiles covering the compressed span
   uint64_t span = 0;       // compressed time span (last compressed time + 1)
+  uint32_t gap_cap = 64;   // gap compression cap of the current bitmap (> every high)
   uint32_t* d_occ = nullptr;
   size_t occ_bytes = 0;
+  uint32_t* d_types_raw = nullptr;  // validated SoA kept for bitmap rebuilds
+  int64_t* d_times_raw = nullptr;
+  uint64_t raw_cap = 0;
   uint64_t launches = 0;   // kernels launched by loads (stats)
   std::vector<uint64_t> type_hist;  // events per type (a_pad entries; matched-pair model)
 
   ~DeviceStream() { release(); }
   void release();
-  void load(const uint32_t* d_types, const int64_t* d_times, uint64_t n_events, uint32_t alphabet,
-            cudaStream_t st, DeviceScratch& scratch);
+  // Caller fills d_types_raw / d_times_raw (n_events entries) then calls load.
+  void reserve_raw(uint64_t n_events);
+  void load(uint64_t n_events, uint32_t alphabet, cudaStream_t st, DeviceScratch& scratch);
+  // Rebuild the bitmap with a larger gap cap when a batch has high >= gap_cap.
+  void ensure_cap(int64_t max_high, cudaStream_t st, DeviceScratch& scratch);
 
  private:
+  void build(uint64_t n_events, uint32_t cap, bool validate, cudaStream_t st, DeviceScratch& scratch);
   void ensure_occ(uint64_t tiles, cudaStream_t st);
 };
 

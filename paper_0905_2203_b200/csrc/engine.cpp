@@ -107,16 +107,21 @@ void Engine::h2d(void* dst, const void* src, size_t bytes) {
 void Engine::load_stream_host(const uint32_t* types, const int64_t* times, uint64_t n,
                               uint32_t alphabet) {
   if (n && (!types || !times)) throw Error(EPI_EINVAL, "epi_load_stream: null event arrays");
-  uint32_t* d_types = scratch_.get<uint32_t>(6, n);
-  int64_t* d_times = scratch_.get<int64_t>(7, n);
-  h2d(d_types, types, n * sizeof(uint32_t));
-  h2d(d_times, times, n * sizeof(int64_t));
-  stream_.load(d_types, d_times, n, alphabet, st_, scratch_);
+  stream_.reserve_raw(n);
+  h2d(stream_.d_types_raw, types, n * sizeof(uint32_t));
+  h2d(stream_.d_times_raw, times, n * sizeof(int64_t));
+  stream_.load(n, alphabet, st_, scratch_);
 }
 
 void Engine::load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,
                                 uint32_t alphabet) {
-  stream_.load(d_types, d_times, n, alphabet, st_, scratch_);
+  if (n && (!d_types || !d_times)) throw Error(EPI_EINVAL, "epi_load_stream_device: null arrays");
+  stream_.reserve_raw(n);
+  EPI_CUDA(cudaMemcpyAsync(stream_.d_types_raw, d_types, n * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, st_));
+  EPI_CUDA(cudaMemcpyAsync(stream_.d_times_raw, d_times, n * sizeof(int64_t),
+                           cudaMemcpyDeviceToDevice, st_));
+  stream_.load(n, alphabet, st_, scratch_);
 }
 
 void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
@@ -144,6 +149,8 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
   uint32_t* h_win = reinterpret_cast<uint32_t*>(host + off_win);
   uint32_t* h_sigma = reinterpret_cast<uint32_t*>(host + off_sigma);
   const uint32_t A = stream_.alphabet;
+  int64_t max_high = 0;
+  int64_t width = -1;  // launch-uniform window width high-low, 0 if mixed
   for (size_t e = 0; e < n; ++e) {
     for (uint32_t k = 0; k < N; ++k) {
       uint32_t t = set.types[e * N + k];
@@ -152,25 +159,37 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
     uint32_t sig = 0;
     for (uint32_t k = 0; k < M; ++k) {
       int64_t lo = set.lo[e * M + k], hi = set.hi[e * M + k];
-      if (hi > kMaxHigh)
-        throw Error(EPI_EUNSUPPORTED,
-                    "constraint high > 63 is not supported on the bit-sliced device path");
-      h_win[e * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 8);
+      if (hi > kMaxHighWide)
+        throw Error(EPI_EUNSUPPORTED, "constraint high > 4095 ms is not supported by the device counter");
+      h_win[e * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
       sig += static_cast<uint32_t>(hi);
+      max_high = std::max(max_high, hi);
+      if (width == -1)
+        width = hi - lo;
+      else if (width != hi - lo)
+        width = 0;
     }
     h_sigma[e] = sig;
     max_sigma = std::max(max_sigma, sig);
   }
+  // Wide windows need a bitmap whose gap compression cap exceeds them, and
+  // the local-memory history ring (hist_words 32 ms words per position).
+  const bool wide = max_high > kMaxHigh;
+  if (wide) stream_.ensure_cap(max_high, st_, scratch_);
+  const int32_t hist_words = wide ? static_cast<int32_t>((max_high + 31) / 32) : 2;
 
   // MapConcatenate plan: enough (episode, segment) machines to fill the GPU,
   // segments long enough that each window lies inside the previous segment.
   const int64_t n_tiles = static_cast<int64_t>(stream_.n_tiles);
   const int32_t window_tiles = static_cast<int32_t>((max_sigma + 31) / 32 + 1);
-  const int64_t min_seg = std::max<int64_t>(window_tiles * 4, 8);
+  // The concat walk is sequential in P, so P is capped (kMaxWalkSegments);
+  // segments of >= 32 tiles keep the window overhead and patch rate low.
+  constexpr int64_t kMaxWalkSegments = 128;
+  const int64_t min_seg = std::max<int64_t>(window_tiles * 4, 32);
   const int64_t target = static_cast<int64_t>(num_sms_) * 2048;
   int64_t want = (target + static_cast<int64_t>(n) - 1) / static_cast<int64_t>(n);
   int64_t max_p = std::max<int64_t>(1, n_tiles / min_seg);
-  int64_t P = std::clamp<int64_t>(want, 1, std::min<int64_t>(max_p, 65535));
+  int64_t P = std::clamp<int64_t>(want, 1, std::min<int64_t>(max_p, kMaxWalkSegments));
   if (const char* force = std::getenv("EPI_FORCE_SEGMENTS")) {
     // Test knob: many short segments exercise the concat walk on small
     // streams. Correctness only needs each segment to span sum(high).
@@ -213,10 +232,18 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
   p.counts = d_counts;
   p.patches = reinterpret_cast<unsigned long long*>(d_counts + n);
 
+  p.hist_words = hist_words;
+
   EPI_CUDA(cudaEventRecord(ev0_, st_));
-  launch_machines(static_cast<int>(N), p, st_);
+  if (wide)
+    launch_machines_wide(static_cast<int>(N), p, st_);
+  else
+    launch_machines(static_cast<int>(N), width > 0 ? static_cast<int>(width) : 0, p, st_);
   EPI_CUDA(cudaEventRecord(ev2_, st_));
-  launch_walk(static_cast<int>(N), p, st_);
+  if (wide)
+    launch_walk_wide(static_cast<int>(N), p, st_);
+  else
+    launch_walk(static_cast<int>(N), p, st_);
   EPI_CUDA(cudaEventRecord(ev1_, st_));
 
   uint64_t* h_counts = static_cast<uint64_t*>(pin_down_.get((n + 1) * sizeof(uint64_t)));

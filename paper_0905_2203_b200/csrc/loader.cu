@@ -37,17 +37,17 @@ constexpr int kLoadThreads = 256;
 constexpr int kLoadItems = 8;
 constexpr int kLoadTile = kLoadThreads * kLoadItems;
 
-__device__ __forceinline__ uint32_t capped_gap(const int64_t* times, uint64_t i) {
+__device__ __forceinline__ uint32_t capped_gap(const int64_t* times, uint64_t i, uint32_t cap) {
   if (i == 0) return 0;
   int64_t d = times[i] - times[i - 1];
-  return d >= kGapCap ? static_cast<uint32_t>(kGapCap) : static_cast<uint32_t>(d);
+  return d >= cap ? cap : static_cast<uint32_t>(d);
 }
 
 // Pass 1. err_key = min over bad events of (index*4 + check), check order as
 // in from_events: 0 negative time, 1 time regression, 2 type out of range.
 __global__ void __launch_bounds__(kLoadThreads)
     validate_reduce_kernel(const uint32_t* __restrict__ types, const int64_t* __restrict__ times,
-                           uint64_t n, uint32_t alphabet, unsigned long long* err_key,
+                           uint64_t n, uint32_t alphabet, uint32_t cap, unsigned long long* err_key,
                            uint64_t* block_sums) {
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kLoadTile;
   uint32_t sum = 0;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kLoadThreads)
       else if (types[i] >= alphabet)
         key = i * 4 + 2;
       if (key < bad) bad = key;
-      if (key == ~0ull) sum += capped_gap(times, i);
+      if (key == ~0ull) sum += capped_gap(times, i, cap);
     }
   }
   if (bad != ~0ull) atomicMin(err_key, bad);
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(1024) scan_block_sums_kernel(uint64_t* block_s
 // a thread-serial prefix plus one block-wide scan of thread totals.
 __global__ void __launch_bounds__(kLoadThreads)
     scan_bitmap_kernel(const uint32_t* __restrict__ types, const int64_t* __restrict__ times,
-                       uint64_t n, const uint64_t* __restrict__ block_offsets, uint32_t a_pad,
+                       uint64_t n, uint32_t cap, const uint64_t* __restrict__ block_offsets, uint32_t a_pad,
                        uint32_t* __restrict__ occ, unsigned long long* __restrict__ hist,
                        bool smem_hist) {
   extern __shared__ uint32_t s_hist[];
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kLoadThreads)
 #pragma unroll
   for (int j = 0; j < kLoadItems; ++j) {
     uint64_t i = base + j;
-    gaps[j] = i < n ? capped_gap(times, i) : 0;
+    gaps[j] = i < n ? capped_gap(times, i, cap) : 0;
     run += gaps[j];
   }
   using Scan = cub::BlockScan<uint32_t, kLoadThreads>;
@@ -150,29 +150,62 @@ void DeviceStream::release() {
   if (d_occ) cudaFree(d_occ);
   d_occ = nullptr;
   occ_bytes = 0;
+  if (d_types_raw) cudaFree(d_types_raw);
+  if (d_times_raw) cudaFree(d_times_raw);
+  d_types_raw = nullptr;
+  d_times_raw = nullptr;
+  raw_cap = 0;
 }
 
-void DeviceStream::load(const uint32_t* d_types, const int64_t* d_times, uint64_t n_events,
-                        uint32_t alphabet_size, cudaStream_t st, DeviceScratch& scratch) {
+void DeviceStream::reserve_raw(uint64_t n_events) {
+  if (n_events <= raw_cap) return;
+  if (d_types_raw) cudaFree(d_types_raw);
+  if (d_times_raw) cudaFree(d_times_raw);
+  d_types_raw = nullptr;
+  d_times_raw = nullptr;
+  raw_cap = 0;
+  EPI_CUDA(cudaMalloc(&d_types_raw, n_events * sizeof(uint32_t)));
+  EPI_CUDA(cudaMalloc(&d_times_raw, n_events * sizeof(int64_t)));
+  raw_cap = n_events;
+}
+
+void DeviceStream::load(uint64_t n_events, uint32_t alphabet_size, cudaStream_t st,
+                        DeviceScratch& scratch) {
   n = 0;
   alphabet = alphabet_size;
   // One spare always-zero column (index `alphabet`) for episode types that
   // lie outside the alphabet and therefore never fire.
   a_pad = (alphabet_size + 1 + 3) / 4 * 4;
+  build(n_events, static_cast<uint32_t>(kGapCap), true, st, scratch);
+}
+
+void DeviceStream::ensure_cap(int64_t max_high, cudaStream_t st, DeviceScratch& scratch) {
+  if (max_high < static_cast<int64_t>(gap_cap)) return;
+  // Smallest multiple of the tile width above max_high.
+  const uint32_t cap = static_cast<uint32_t>((max_high + 1 + 31) / 32 * 32);
+  build(n, cap, false, st, scratch);
+}
+
+void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStream_t st,
+                         DeviceScratch& scratch) {
+  gap_cap = cap;
   n_tiles = 1;
   if (n_events == 0) {
     // An empty stream still gets one (zero) tile so kernels need no special case.
     ensure_occ(1, st);
     type_hist.assign(a_pad, 0);
     n = 0;
+    span = 0;
     return;
   }
+  const uint32_t* d_types = d_types_raw;
+  const int64_t* d_times = d_times_raw;
   const uint64_t nb = (n_events + kLoadTile - 1) / kLoadTile;
   uint64_t* d_sums = scratch.get<uint64_t>(0, nb + 1);
   unsigned long long* d_err = scratch.get<unsigned long long>(1, 1);
   EPI_CUDA(cudaMemsetAsync(d_err, 0xff, sizeof(unsigned long long), st));
   validate_reduce_kernel<<<static_cast<unsigned>(nb), kLoadThreads, 0, st>>>(
-      d_types, d_times, n_events, alphabet_size, d_err, d_sums);
+      d_types, d_times, n_events, alphabet, cap, d_err, d_sums);
   EPI_CUDA(cudaGetLastError());
   scan_block_sums_kernel<<<1, 1024, 0, st>>>(d_sums, nb);
   EPI_CUDA(cudaGetLastError());
@@ -182,7 +215,7 @@ void DeviceStream::load(const uint32_t* d_types, const int64_t* d_times, uint64_
   EPI_CUDA(cudaMemcpyAsync(&h_total, d_sums + nb, sizeof h_total, cudaMemcpyDeviceToHost, st));
   EPI_CUDA(cudaStreamSynchronize(st));
   launches += 2;
-  if (h_err != ~0ull) {
+  if (validate && h_err != ~0ull) {
     static const char* kMsg[3] = {"negative event time", "event times must be non-decreasing",
                                   "event type id out of range"};
     throw Error(2 /*EPI_EDATA*/, kMsg[h_err & 3]);
@@ -195,11 +228,12 @@ void DeviceStream::load(const uint32_t* d_types, const int64_t* d_times, uint64_
   EPI_CUDA(cudaMemsetAsync(d_hist, 0, a_pad * sizeof(unsigned long long), st));
   const bool smem_hist = a_pad <= 8192;
   scan_bitmap_kernel<<<static_cast<unsigned>(nb), kLoadThreads, smem_hist ? a_pad * 4 : 0, st>>>(
-      d_types, d_times, n_events, d_sums, a_pad, d_occ, d_hist, smem_hist);
+      d_types, d_times, n_events, cap, d_sums, a_pad, d_occ, d_hist, smem_hist);
   EPI_CUDA(cudaGetLastError());
   launches += 1;
   type_hist.assign(a_pad, 0);
-  EPI_CUDA(cudaMemcpyAsync(type_hist.data(), d_hist, a_pad * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  EPI_CUDA(cudaMemcpyAsync(type_hist.data(), d_hist, a_pad * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost, st));
   EPI_CUDA(cudaStreamSynchronize(st));
   n = n_events;
   n_tiles = tiles;
@@ -210,7 +244,9 @@ void DeviceStream::ensure_occ(uint64_t tiles, cudaStream_t st) {
   // Pad the allocation so staged chunk reads never run past the end.
   const size_t need = (tiles + 1) * static_cast<size_t>(a_pad) * sizeof(uint32_t);
   if (need > occ_bytes) {
-    release();
+    if (d_occ) cudaFree(d_occ);
+    d_occ = nullptr;
+    occ_bytes = 0;
     EPI_CUDA(cudaMalloc(&d_occ, need));
     occ_bytes = need;
   }

@@ -141,7 +141,29 @@ def test_errors(ctx):
     with pytest.raises(InvalidArgument, match="at least one node"):
         ctx.count_csr(csr_of([([], [])]))
     with pytest.raises(Unsupported):
-        ctx.count_csr(csr_of([([0, 1], [(5, 100)])]))
+        ctx.count_csr(csr_of([([0, 1], [(5, 5000)])]))
+
+
+@pytest.mark.parametrize("seed,high_max,gap_max", [(0, 250, 40), (1, 250, 400), (2, 4095, 900),
+                                                   (3, 120, 10)])
+def test_random_wide_windows_vs_port(ctx, seed, high_max, gap_max, segments_env):
+    """Constraints with high > 63 take the wide-window kernels (local-memory
+    history ring, bitmap rebuilt with a larger gap-compression cap)."""
+    rng = np.random.default_rng(5000 + seed)
+    for it in range(25):
+        segments_env([None, 2, 5][it % 3])
+        types, times, a, eps = _random_case(rng, 2500, 6, gap_max, 6, high_max)
+        got = count_one(ctx, types, times, a, eps)
+        csr = csr_of(eps)
+        want = oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=4)
+        np.testing.assert_array_equal(got, want, err_msg=f"seed {seed} it {it}")
+        # mixing back to a narrow batch on the same (rebuilt) bitmap stays exact
+        narrow = [(t, [(lo % 40, min(hi, 63)) if lo % 40 < min(hi, 63) else (0, 5) for lo, hi in c])
+                  for t, c in eps]
+        got2 = ctx.count_csr(csr_of(narrow))
+        csr2 = csr_of(narrow)
+        want2 = oracle.count_batch(types, times, csr2.offsets, csr2.types, csr2.low, csr2.high, threads=4)
+        np.testing.assert_array_equal(got2, want2, err_msg=f"narrow seed {seed} it {it}")
 
 
 def _gen(name):
