@@ -56,6 +56,7 @@ struct DeviceStream {
   uint64_t raw_cap = 0;
   uint64_t launches = 0;   // kernels launched by loads (stats)
   std::vector<uint64_t> type_hist;  // events per type (a_pad entries; matched-pair model)
+  unsigned long long* d_hist = nullptr;  // device copy of type_hist (scratch-owned)
 
   ~DeviceStream() { release(); }
   void release();

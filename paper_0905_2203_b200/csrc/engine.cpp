@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 #include <unordered_map>
 
 #include "count.h"
@@ -22,9 +23,11 @@ namespace epi {
 namespace {
 
 enum Slot : size_t {
+  // 0..2 belong to the loader
   kSlotParams = 3,
   kSlotMachines = 4,
   kSlotCounts = 5,
+  kSlotSegments = 6,
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;
@@ -48,6 +51,21 @@ uint64_t hash_span(const uint32_t* t, size_t nt, const int64_t* lo, const int64_
     mix(static_cast<uint64_t>(hi[i]));
   }
   return h;
+}
+
+// Split [0, n) into contiguous chunks over host threads (inline when small).
+template <class F>
+void host_parallel(size_t n, bool big, F&& f) {
+  unsigned w = std::thread::hardware_concurrency();
+  w = std::min<unsigned>(w ? w : 1, 32);
+  if (!big || w <= 1 || n < 2 * w) {
+    f(size_t{0}, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned i = 1; i < w; ++i) th.emplace_back([&, i] { f(n * i / w, n * (i + 1) / w); });
+  f(size_t{0}, n / w);
+  for (auto& t : th) t.join();
 }
 
 }  // namespace
@@ -139,17 +157,15 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
   const size_t off_types = 0;
   const size_t off_win = align_up(off_types + n * N * 4, 256);
   const size_t off_sigma = align_up(off_win + n * M * 4, 256);
-  const size_t off_seg = align_up(off_sigma + n * 4, 256);
-  uint32_t max_sigma = 0;
-  // Segment plan needs max_sigma; compute parameters first into pinned memory.
-  const size_t seg_cap = 65536 + 1;
-  const size_t total = align_up(off_seg + seg_cap * 4, 256);
+  const size_t total = align_up(off_sigma + n * 4, 256);
   char* host = static_cast<char*>(pin_up_.get(total));
   uint32_t* h_types = reinterpret_cast<uint32_t*>(host + off_types);
   uint32_t* h_win = reinterpret_cast<uint32_t*>(host + off_win);
   uint32_t* h_sigma = reinterpret_cast<uint32_t*>(host + off_sigma);
+  DevSet ds;
+  ds.N = N;
+  ds.n = n;
   const uint32_t A = stream_.alphabet;
-  int64_t max_high = 0;
   int64_t width = -1;  // launch-uniform window width high-low, 0 if mixed
   for (size_t e = 0; e < n; ++e) {
     for (uint32_t k = 0; k < N; ++k) {
@@ -163,24 +179,49 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
         throw Error(EPI_EUNSUPPORTED, "constraint high > 4095 ms is not supported by the device counter");
       h_win[e * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
       sig += static_cast<uint32_t>(hi);
-      max_high = std::max(max_high, hi);
+      ds.max_high = std::max(ds.max_high, hi);
       if (width == -1)
         width = hi - lo;
       else if (width != hi - lo)
         width = 0;
     }
     h_sigma[e] = sig;
-    max_sigma = std::max(max_sigma, sig);
+    ds.max_sigma = std::max(ds.max_sigma, sig);
   }
+  ds.width = width > 0 ? static_cast<int>(width) : 0;
+  char* d_params = scratch_.get<char>(kSlotParams, total);
+  EPI_CUDA(cudaMemcpyAsync(d_params, host, total, cudaMemcpyHostToDevice, st_));
+  stats.h2d_bytes += total;
+  ds.types = reinterpret_cast<const uint32_t*>(d_params + off_types);
+  ds.win = reinterpret_cast<const uint32_t*>(d_params + off_win);
+  ds.sigma = reinterpret_cast<const uint32_t*>(d_params + off_sigma);
+
+  uint64_t* d_counts = scratch_.get<uint64_t>(kSlotCounts, n);
+  count_device(ds, d_counts, stats, ms_out);
+  uint64_t* h_counts = static_cast<uint64_t*>(pin_down_.get(n * sizeof(uint64_t)));
+  EPI_CUDA(cudaMemcpyAsync(h_counts, d_counts, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaStreamSynchronize(st_));
+  std::memcpy(counts.data(), h_counts, n * sizeof(uint64_t));
+  stats.d2h_bytes += n * sizeof(uint64_t);
+}
+
+// Exact counts of a device-resident set into d_counts (device). Plans the
+// MapConcatenate segments, launches the map and concat-walk kernels, and
+// waits for them (stats need the patch counter and the event times).
+void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out) {
+  const size_t n = ds.n;
+  if (n == 0) return;
+  const uint32_t N = ds.N;
   // Wide windows need a bitmap whose gap compression cap exceeds them, and
   // the local-memory history ring (hist_words 32 ms words per position).
-  const bool wide = max_high > kMaxHigh;
-  if (wide) stream_.ensure_cap(max_high, st_, scratch_);
-  const int32_t hist_words = wide ? static_cast<int32_t>((max_high + 31) / 32) : 2;
+  const bool wide = ds.max_high > kMaxHigh;
+  if (wide) stream_.ensure_cap(ds.max_high, st_, scratch_);
+  const int32_t hist_words = wide ? static_cast<int32_t>((ds.max_high + 31) / 32) : 2;
 
   // MapConcatenate plan: enough (episode, segment) machines to fill the GPU,
   // segments long enough that each window lies inside the previous segment.
   const int64_t n_tiles = static_cast<int64_t>(stream_.n_tiles);
+  const uint32_t max_sigma = ds.max_sigma;
   const int32_t window_tiles = static_cast<int32_t>((max_sigma + 31) / 32 + 1);
   // The concat walk is sequential in P, so P is capped (kMaxWalkSegments);
   // segments of >= 32 tiles keep the window overhead and patch rate low.
@@ -194,81 +235,73 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
     // Test knob: many short segments exercise the concat walk on small
     // streams. Correctness only needs each segment to span sum(high).
     const int64_t min_ok = std::max<int64_t>(1, (max_sigma + 31) / 32);
-    P = std::clamp<int64_t>(std::atoll(force), 1, std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
+    P = std::clamp<int64_t>(std::atoll(force), 1,
+                            std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
   }
   const int64_t seg_len = (n_tiles + P - 1) / P;
   P = (n_tiles + seg_len - 1) / seg_len;
-  int32_t* h_seg = reinterpret_cast<int32_t*>(host + off_seg);
+  int32_t* h_seg = static_cast<int32_t*>(pin_seg_.get((P + 1) * sizeof(int32_t)));
   for (int64_t q = 0; q < P; ++q) h_seg[q] = static_cast<int32_t>(q * seg_len);
   h_seg[P] = static_cast<int32_t>(n_tiles);
-  const size_t upload = off_seg + (P + 1) * 4;
-
-  char* d_params = scratch_.get<char>(kSlotParams, upload);
-  EPI_CUDA(cudaMemcpyAsync(d_params, host, upload, cudaMemcpyHostToDevice, st_));
+  int32_t* d_seg = scratch_.get<int32_t>(kSlotSegments, P + 1 + 6);
+  EPI_CUDA(cudaMemcpyAsync(d_seg, h_seg, (P + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+  unsigned long long* d_patch = reinterpret_cast<unsigned long long*>(d_seg + ((P + 2) & ~1));
+  EPI_CUDA(cudaMemsetAsync(d_patch, 0, 2 * sizeof(unsigned long long), st_));
+  // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k).
+  launch_matched_pairs(ds.types, n * N, stream_.d_hist, d_patch + 1, st_);
 
   const size_t nm = static_cast<size_t>(P) * n;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
                m_first = align_up(m_last + nm * 8, 256), m_total = m_first + nm * 8 * kRecorded;
   char* d_mach = scratch_.get<char>(kSlotMachines, m_total);
-  uint64_t* d_counts = scratch_.get<uint64_t>(kSlotCounts, n + 1);
-  EPI_CUDA(cudaMemsetAsync(d_counts + n, 0, sizeof(uint64_t), st_));
 
   CountLaunch p{};
   p.occ = stream_.d_occ;
   p.a_pad = stream_.a_pad;
   p.n_tiles = static_cast<int32_t>(n_tiles);
-  p.seg_g = reinterpret_cast<const int32_t*>(d_params + off_seg);
+  p.seg_g = d_seg;
   p.P = static_cast<int32_t>(P);
   p.window_tiles = window_tiles;
   p.chunk_tiles = static_cast<int32_t>(chunk_tiles_for(stream_.a_pad));
+  p.hist_words = hist_words;
   p.n_eps = static_cast<uint32_t>(n);
-  p.ep_types = reinterpret_cast<const uint32_t*>(d_params + off_types);
-  p.ep_win = reinterpret_cast<const uint32_t*>(d_params + off_win);
-  p.ep_sigma = reinterpret_cast<const uint32_t*>(d_params + off_sigma);
+  p.ep_types = ds.types;
+  p.ep_win = ds.win;
+  p.ep_sigma = ds.sigma;
   p.f_count = reinterpret_cast<uint32_t*>(d_mach + m_count);
   p.f_ncomp = reinterpret_cast<uint32_t*>(d_mach + m_ncomp);
   p.f_last = reinterpret_cast<uint64_t*>(d_mach + m_last);
   p.f_first = reinterpret_cast<uint64_t*>(d_mach + m_first);
   p.counts = d_counts;
-  p.patches = reinterpret_cast<unsigned long long*>(d_counts + n);
-
-  p.hist_words = hist_words;
+  p.patches = d_patch;
 
   EPI_CUDA(cudaEventRecord(ev0_, st_));
   if (wide)
     launch_machines_wide(static_cast<int>(N), p, st_);
   else
-    launch_machines(static_cast<int>(N), width > 0 ? static_cast<int>(width) : 0, p, st_);
+    launch_machines(static_cast<int>(N), ds.width, p, st_);
   EPI_CUDA(cudaEventRecord(ev2_, st_));
   if (wide)
     launch_walk_wide(static_cast<int>(N), p, st_);
   else
     launch_walk(static_cast<int>(N), p, st_);
   EPI_CUDA(cudaEventRecord(ev1_, st_));
-
-  uint64_t* h_counts = static_cast<uint64_t*>(pin_down_.get((n + 1) * sizeof(uint64_t)));
-  EPI_CUDA(cudaMemcpyAsync(h_counts, d_counts, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                           st_));
+  unsigned long long h_patch[2] = {0, 0};
+  EPI_CUDA(cudaMemcpyAsync(h_patch, d_patch, sizeof h_patch, cudaMemcpyDeviceToHost, st_));
   EPI_CUDA(cudaStreamSynchronize(st_));
   float ms = 0, map_ms = 0;
   EPI_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
   EPI_CUDA(cudaEventElapsedTime(&map_ms, ev0_, ev2_));
-  std::memcpy(counts.data(), h_counts, n * sizeof(uint64_t));
-  stats.patches += h_counts[n];
+  stats.patches += h_patch[0];
   stats.segments = static_cast<uint64_t>(P);
   stats.kernel_launches += 2;
   stats.map_launches += 1;
   stats.total_ms += ms;
   stats.map_ms += map_ms;
   stats.concat_ms += ms - map_ms;
-  stats.h2d_bytes += upload;
-  stats.d2h_bytes += (n + 1) * sizeof(uint64_t);
+  stats.h2d_bytes += (P + 1) * sizeof(int32_t);
   stats.episode_events += static_cast<uint64_t>(n) * stream_.n;
-  // Matched-pair work model: every event of every episode position's type.
-  uint64_t matched = 0;
-  for (size_t e = 0; e < n; ++e)
-    for (uint32_t k = 0; k < N; ++k) matched += stream_.type_hist[h_types[e * N + k]];
-  stats.matched_pairs += matched;
+  stats.matched_pairs += h_patch[1];
   uint64_t tiles = 0;
   for (int64_t q = 0; q < P; ++q)
     tiles += static_cast<uint64_t>(h_seg[q + 1] - std::max<int64_t>(h_seg[q] - window_tiles, 0));
@@ -292,26 +325,33 @@ void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
   // count(hull) >= count(variant): a sound upper bound. Singleton groups are
   // exact already.
   const uint32_t N = set.N, M = N - 1;
-  std::unordered_map<uint64_t, std::vector<uint32_t>> buckets;
-  buckets.reserve(n);
+  // Open-addressing table keyed by the type-sequence hash; slots hold group
+  // ids, collisions are resolved by comparing the stored type sequence.
+  size_t cap = 1;
+  while (cap < 2 * n) cap <<= 1;
+  std::vector<uint32_t> table(cap, UINT32_MAX);
   std::vector<uint32_t> group(n);
   EpisodeSet relaxed;
   relaxed.N = N;
+  relaxed.types.reserve(n * N / 4 + N);
   std::vector<uint32_t> gsize;
   std::vector<uint32_t> grep;
   for (size_t i = 0; i < n; ++i) {
     const uint32_t* t = &set.types[i * N];
     uint64_t h = hash_span(t, N, nullptr, nullptr, 0);
-    auto& cand = buckets[h];
+    size_t slot = static_cast<size_t>(h ^ (h >> 29)) & (cap - 1);
     uint32_t g = UINT32_MAX;
-    for (uint32_t gi : cand)
+    while (table[slot] != UINT32_MAX) {
+      const uint32_t gi = table[slot];
       if (std::memcmp(&relaxed.types[static_cast<size_t>(gi) * N], t, N * 4) == 0) {
         g = gi;
         break;
       }
+      slot = (slot + 1) & (cap - 1);
+    }
     if (g == UINT32_MAX) {
       g = static_cast<uint32_t>(gsize.size());
-      cand.push_back(g);
+      table[slot] = g;
       relaxed.types.insert(relaxed.types.end(), t, t + N);
       relaxed.lo.insert(relaxed.lo.end(), &set.lo[i * M], &set.lo[i * M] + M);
       relaxed.hi.insert(relaxed.hi.end(), &set.hi[i * M], &set.hi[i * M] + M);
@@ -401,10 +441,13 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
 }
 
 // generate_candidates (E/miner.hpp:76-109). `frequent` holds the level-1
-// frequent episodes in candidate order; the join key of the reference
-// (episode_key, E/miner.hpp:52-68: types and constraints of a contiguous
-// slice) is hashed and verified, and the output order is the reference's:
-// lefts in frequent order, rights in bucket (frequent) order.
+// frequent episodes in candidate order. The reference joins through a
+// string-keyed hash of episode_key (E/miner.hpp:52-68: types and constraints
+// of a contiguous slice); here the key is a 64-bit hash, the prefix keys are
+// stably sorted once, each left's suffix key is binary-searched and verified,
+// and the output is sized by a count pass and filled in parallel. The output
+// order is the reference's: lefts in frequent order, rights in bucket
+// (frequent) order.
 void generate_candidates(size_t level, const EpisodeSet& frequent,
                          const std::vector<std::pair<int64_t, int64_t>>& alphabet,
                          uint32_t alphabet_size, EpisodeSet& out) {
@@ -418,14 +461,19 @@ void generate_candidates(size_t level, const EpisodeSet& frequent,
   const size_t nf = frequent.size();
   if (nf == 0) return;
   if (level == 2) {
-    out.types.reserve(nf * nf * alphabet.size() * 2);
+    const size_t na = alphabet.size(), total = nf * nf * na;
+    out.types.resize(total * 2);
+    out.lo.resize(total);
+    out.hi.resize(total);
+    size_t o = 0;
     for (size_t l = 0; l < nf; ++l)
       for (size_t r = 0; r < nf; ++r)
         for (const auto& c : alphabet) {
-          out.types.push_back(frequent.types[l]);
-          out.types.push_back(frequent.types[r]);
-          out.lo.push_back(c.first);
-          out.hi.push_back(c.second);
+          out.types[2 * o] = frequent.types[l];
+          out.types[2 * o + 1] = frequent.types[r];
+          out.lo[o] = c.first;
+          out.hi[o] = c.second;
+          ++o;
         }
     return;
   }
@@ -445,87 +493,46 @@ void generate_candidates(size_t level, const EpisodeSet& frequent,
         return false;
     return true;
   };
-  std::unordered_map<uint64_t, std::vector<uint32_t>> by_prefix;
-  by_prefix.reserve(nf * 2);
-  for (size_t i = 0; i < nf; ++i) by_prefix[key_hash(i, 0)].push_back(static_cast<uint32_t>(i));
+  // (prefix key, index) sorted: equal keys keep frequent order.
+  std::vector<std::pair<uint64_t, uint32_t>> pre(nf);
+  for (size_t i = 0; i < nf; ++i) pre[i] = {key_hash(i, 0), static_cast<uint32_t>(i)};
+  std::sort(pre.begin(), pre.end());
+  std::vector<uint32_t> lo_at(nf), hi_at(nf);  // bucket range per left
+  std::vector<uint64_t> off(nf + 1, 0);
   for (size_t l = 0; l < nf; ++l) {
-    auto it = by_prefix.find(key_hash(l, 1));
-    if (it == by_prefix.end()) continue;
-    for (uint32_t r : it->second) {
-      if (!key_eq(r, 0, l, 1)) continue;
-      out.types.insert(out.types.end(), &frequent.types[l * F], &frequent.types[l * F] + F);
-      out.types.push_back(frequent.types[static_cast<size_t>(r) * F + F - 1]);
-      out.lo.insert(out.lo.end(), &frequent.lo[l * FM], &frequent.lo[l * FM] + FM);
-      out.hi.insert(out.hi.end(), &frequent.hi[l * FM], &frequent.hi[l * FM] + FM);
-      out.lo.push_back(frequent.lo[static_cast<size_t>(r) * FM + FM - 1]);
-      out.hi.push_back(frequent.hi[static_cast<size_t>(r) * FM + FM - 1]);
-    }
+    const uint64_t h = key_hash(l, 1);
+    auto r0 = std::lower_bound(pre.begin(), pre.end(), std::make_pair(h, 0u));
+    auto r1 = std::upper_bound(r0, pre.end(), std::make_pair(h, UINT32_MAX));
+    lo_at[l] = static_cast<uint32_t>(r0 - pre.begin());
+    hi_at[l] = static_cast<uint32_t>(r1 - pre.begin());
+    uint64_t c = 0;
+    for (auto it = r0; it != r1; ++it) c += key_eq(it->second, 0, l, 1);
+    off[l + 1] = off[l] + c;
   }
-}
-
-// mine (E/miner.hpp:114-173) with the counting block replaced by one
-// device count per level.
-void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
-  if (cfg.threshold < 1) throw Error(EPI_EINVAL, "mine: threshold must be >= 1");
-  if (cfg.max_level < 1) throw Error(EPI_EINVAL, "mine: max_level must be >= 1");
-  if (cfg.n_alpha == 0) throw Error(EPI_EINVAL, "mine: constraint alphabet must not be empty");
-  std::vector<std::pair<int64_t, int64_t>> alpha;
-  for (uint64_t i = 0; i < cfg.n_alpha; ++i) {
-    validate_constraint(cfg.alpha_low[i], cfg.alpha_high[i]);
-    alpha.emplace_back(cfg.alpha_low[i], cfg.alpha_high[i]);
-  }
-  m_level_cands_.clear();
-  m_level_off_.assign(1, 0);
-  m_level_ms_.clear();
-  m_counts_.clear();
-  m_off_.assign(1, 0);
-  m_types_.clear();
-  m_lo_.clear();
-  m_hi_.clear();
-  epi_stats totals{};
-
-  EpisodeSet frequent, cands;
-  std::vector<uint64_t> counts;
-  for (size_t level = 1; level <= cfg.max_level; ++level) {
-    auto t0 = std::chrono::steady_clock::now();
-    generate_candidates(level, frequent, alpha, stream_.alphabet, cands);
-    const size_t nc = cands.size();
-    if (nc == 0) break;
-    count_set(cands, cfg.threshold, level == 1 ? EPI_MODE_EXACT : cfg.mode, counts, totals);
-    EpisodeSet next;
-    next.N = cands.N;
-    const uint32_t N = cands.N, M = N - 1;
-    for (size_t i = 0; i < nc; ++i) {
-      if (counts[i] == kPruned || counts[i] < cfg.threshold) continue;
-      next.types.insert(next.types.end(), &cands.types[i * N], &cands.types[i * N] + N);
-      next.lo.insert(next.lo.end(), &cands.lo[i * M], &cands.lo[i * M] + M);
-      next.hi.insert(next.hi.end(), &cands.hi[i * M], &cands.hi[i * M] + M);
-      m_counts_.push_back(counts[i]);
-      for (uint32_t k = 0; k < N; ++k) m_types_.push_back(cands.types[i * N + k]);
-      for (uint32_t k = 0; k < M; ++k) {
-        m_lo_.push_back(cands.lo[i * M + k]);
-        m_hi_.push_back(cands.hi[i * M + k]);
+  const size_t total = off[nf];
+  out.types.resize(total * level);
+  out.lo.resize(total * (level - 1));
+  out.hi.resize(total * (level - 1));
+  auto fill = [&](size_t l0, size_t l1) {
+    for (size_t l = l0; l < l1; ++l) {
+      size_t o = off[l];
+      for (uint32_t b = lo_at[l]; b < hi_at[l]; ++b) {
+        const uint32_t r = pre[b].second;
+        if (!key_eq(r, 0, l, 1)) continue;
+        uint32_t* t = &out.types[o * level];
+        std::memcpy(t, &frequent.types[l * F], F * sizeof(uint32_t));
+        t[F] = frequent.types[static_cast<size_t>(r) * F + F - 1];
+        int64_t* lo = &out.lo[o * (level - 1)];
+        int64_t* hi = &out.hi[o * (level - 1)];
+        std::memcpy(lo, &frequent.lo[l * FM], FM * sizeof(int64_t));
+        std::memcpy(hi, &frequent.hi[l * FM], FM * sizeof(int64_t));
+        lo[FM] = frequent.lo[static_cast<size_t>(r) * FM + FM - 1];
+        hi[FM] = frequent.hi[static_cast<size_t>(r) * FM + FM - 1];
+        ++o;
       }
-      m_off_.push_back(static_cast<uint32_t>(m_types_.size()));
     }
-    m_level_cands_.push_back(nc);
-    m_level_off_.push_back(m_counts_.size());
-    m_level_ms_.push_back(
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    frequent = std::move(next);
-    if (frequent.size() == 0) break;
-  }
-  out->n_levels = m_level_cands_.size();
-  out->level_candidates = m_level_cands_.data();
-  out->level_offsets = m_level_off_.data();
-  out->level_ms = m_level_ms_.data();
-  out->frequent.n_episodes = m_counts_.size();
-  out->frequent.offsets = m_off_.data();
-  out->frequent.types = m_types_.data();
-  out->frequent.low = m_lo_.data();
-  out->frequent.high = m_hi_.data();
-  out->counts = m_counts_.data();
-  out->totals = totals;
+  };
+  host_parallel(nf, total * level * 12 > (1u << 20), fill);
 }
 
 }  // namespace epi

@@ -27,6 +27,19 @@ struct EpisodeSet {
   }
 };
 
+// A fixed-length episode set resident on the device, in the counting
+// kernels' parameter layout, plus the host-side summary the launch needs.
+struct DevSet {
+  uint32_t N = 0;
+  uint64_t n = 0;
+  const uint32_t* types = nullptr;  // [n * N]
+  const uint32_t* win = nullptr;    // [n * (N-1)]: (low+1) | high << 16
+  const uint32_t* sigma = nullptr;  // [n] sum of highs
+  uint32_t max_sigma = 0;
+  int64_t max_high = 0;
+  int width = 0;                    // launch-uniform high-low, 0 if mixed
+};
+
 struct PinnedBuffer {
   void* p = nullptr;
   size_t bytes = 0;
@@ -72,6 +85,10 @@ class Engine {
   // Exact count of one fixed-length set on the device.
   void count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                    double* ms_out);
+  void count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out);
+  void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode, uint64_t* d_counts,
+                             epi_stats& stats);
+  uint32_t dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n);
   void h2d(void* dst, const void* src, size_t bytes);
 
   int device_;
@@ -80,7 +97,7 @@ class Engine {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, ev2_ = nullptr;
   DeviceStream stream_;
   DeviceScratch scratch_;
-  PinnedBuffer pin_up_, pin_down_;
+  PinnedBuffer pin_up_, pin_down_, pin_seg_;
 
   // epi_mine result storage
   std::vector<uint64_t> m_level_cands_, m_level_off_, m_counts_;

@@ -194,6 +194,8 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
     // An empty stream still gets one (zero) tile so kernels need no special case.
     ensure_occ(1, st);
     type_hist.assign(a_pad, 0);
+    d_hist = scratch.get<unsigned long long>(2, a_pad);
+    EPI_CUDA(cudaMemsetAsync(d_hist, 0, a_pad * sizeof(unsigned long long), st));
     n = 0;
     span = 0;
     return;
@@ -224,7 +226,7 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
   if (tiles >= (1ull << 31))
     throw Error(7 /*EPI_EUNSUPPORTED*/, "stream spans more than 2^31 compressed time tiles");
   ensure_occ(tiles, st);
-  unsigned long long* d_hist = scratch.get<unsigned long long>(2, a_pad);
+  d_hist = scratch.get<unsigned long long>(2, a_pad);
   EPI_CUDA(cudaMemsetAsync(d_hist, 0, a_pad * sizeof(unsigned long long), st));
   const bool smem_hist = a_pad <= 8192;
   scan_bitmap_kernel<<<static_cast<unsigned>(nb), kLoadThreads, smem_hist ? a_pad * 4 : 0, st>>>(

@@ -1,0 +1,581 @@
+// Device-resident level-wise miner: mine() (E/miner.hpp:114-173) with the
+// candidate join (generate_candidates, E/miner.hpp:76-109), the two-pass
+// elimination and the frequency threshold (E/miner.hpp:159-160) on the GPU.
+// Only the small per-level join index (sorted prefix order + per-left bucket
+// ranges over the FREQUENT set) goes host->device, and only the frequent
+// episodes come back; candidate lists never cross PCIe.
+//
+// Per level L >= 2:
+//   1. generate candidates straight into the counting-kernel parameter layout
+//      (types [n*L], packed windows [n*(L-1)], sum of highs [n]);
+//   2. pass 1 (MINE mode): radix-sort the packed type sequences, one hull
+//      episode per distinct sequence (per position min low, max high), count
+//      the hulls exactly -> a sound upper bound per candidate; prune
+//      bound < threshold; singleton groups are already exact;
+//   3. pass 2: gather the survivors, count them exactly, scatter back;
+//   4. flag count >= threshold, compact in candidate order, copy back.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <chrono>
+#include <numeric>
+
+#include "common.cuh"
+#include "engine.h"
+
+namespace epi {
+namespace {
+
+constexpr uint64_t kPrunedDev = ~0ull;
+
+enum MineSlot : size_t {
+  kMTypes = 10,
+  kMWin,
+  kMSigma,
+  kMCounts,
+  kMFreq,      // frequent set of the previous level (types, win, sigma)
+  kMJoin,      // pre order + per-left ranges + offsets
+  kMKeys,
+  kMKeysAlt,
+  kMIdx,
+  kMIdxAlt,
+  kMFlags,
+  kMScan,
+  kMCub,
+  kMGroups,    // relaxed params + group meta
+  kMGroupCnt,
+  kMSurv,      // survivor params
+  kMSurvCnt,
+  kMOut,       // compacted frequent output
+  kMPruned,
+};
+
+inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+__global__ void gen_level2_kernel(const uint32_t* __restrict__ f1, uint32_t nf1,
+                                  const uint32_t* __restrict__ awin, const uint32_t* __restrict__ ahi,
+                                  uint32_t na, uint32_t* types, uint32_t* win, uint32_t* sigma,
+                                  uint64_t n) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = static_cast<uint32_t>(i % na);
+  const uint64_t lr = i / na;
+  const uint32_t r = static_cast<uint32_t>(lr % nf1), l = static_cast<uint32_t>(lr / nf1);
+  types[2 * i] = f1[l];
+  types[2 * i + 1] = f1[r];
+  win[i] = awin[c];
+  sigma[i] = ahi[c];
+}
+
+// One warp per left: candidates left ++ right.last for every right in the
+// left's bucket (rights sorted by prefix key, stable -> frequent order).
+__global__ void gen_join_kernel(uint32_t L, const uint32_t* __restrict__ ftypes,
+                                const uint32_t* __restrict__ fwin,
+                                const uint32_t* __restrict__ fsigma, uint32_t nf,
+                                const uint32_t* __restrict__ pre, const uint32_t* __restrict__ lrange,
+                                const uint64_t* __restrict__ loff, uint32_t* types, uint32_t* win,
+                                uint32_t* sigma) {
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp >= nf) return;
+  const uint32_t l = warp;
+  const uint32_t F = L - 1, FM = L - 2;
+  const uint32_t b0 = lrange[2 * l], b1 = lrange[2 * l + 1];
+  const uint64_t o0 = loff[l];
+  for (uint32_t b = b0 + lane; b < b1; b += 32) {
+    const uint32_t r = pre[b];
+    const uint64_t o = o0 + (b - b0);
+    uint32_t* t = types + o * L;
+    for (uint32_t k = 0; k < F; ++k) t[k] = ftypes[static_cast<size_t>(l) * F + k];
+    t[F] = ftypes[static_cast<size_t>(r) * F + F - 1];
+    uint32_t* w = win + o * (L - 1);
+    for (uint32_t k = 0; k < FM; ++k) w[k] = fwin[static_cast<size_t>(l) * FM + k];
+    const uint32_t rw = fwin[static_cast<size_t>(r) * FM + FM - 1];
+    w[FM] = rw;
+    sigma[o] = fsigma[l] + (rw >> 16);
+  }
+}
+
+__global__ void pack_keys_kernel(const uint32_t* __restrict__ types, uint32_t L, uint32_t bits,
+                                 uint64_t n, uint64_t* keys, uint32_t* idx) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = 0;
+  for (uint32_t j = 0; j < L; ++j) k = (k << bits) | types[i * L + j];
+  keys[i] = k;
+  idx[i] = static_cast<uint32_t>(i);
+}
+
+__global__ void head_flags_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* flags) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  flags[j] = (j == 0 || keys[j] != keys[j - 1]) ? 1u : 0u;
+}
+
+// scan = exclusive scan of head flags: group of sorted position j is
+// scan[j] + flags[j] - 1; group g starts at the j with flags[j] && scan[j] == g.
+__global__ void group_starts_kernel(const uint32_t* __restrict__ flags,
+                                    const uint32_t* __restrict__ scan, uint64_t n, uint32_t* gstart) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  if (flags[j]) gstart[scan[j]] = static_cast<uint32_t>(j);
+}
+
+// One thread per group: hull of the members' windows.
+__global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* __restrict__ win,
+                            uint32_t L, const uint32_t* __restrict__ idx_sorted,
+                            const uint32_t* __restrict__ gstart, uint32_t n_groups, uint64_t n,
+                            uint32_t* rtypes, uint32_t* rwin, uint32_t* rsigma, uint32_t* gsize) {
+  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const uint32_t j0 = gstart[g];
+  const uint32_t j1 = g + 1 < n_groups ? gstart[g + 1] : static_cast<uint32_t>(n);
+  const uint32_t M = L - 1;
+  const uint32_t first = idx_sorted[j0];
+  for (uint32_t k = 0; k < L; ++k) rtypes[static_cast<size_t>(g) * L + k] = types[static_cast<size_t>(first) * L + k];
+  uint32_t sig = 0;
+  for (uint32_t k = 0; k < M; ++k) {
+    uint32_t lo1 = 0xffffu, hi = 0;
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t w = win[static_cast<size_t>(idx_sorted[j]) * M + k];
+      lo1 = min(lo1, w & 0xffffu);
+      hi = max(hi, w >> 16);
+    }
+    rwin[static_cast<size_t>(g) * M + k] = lo1 | (hi << 16);
+    sig += hi;
+  }
+  rsigma[g] = sig;
+  gsize[g] = j1 - j0;
+}
+
+// Per sorted position: singleton groups are exact, bound < threshold prunes,
+// the rest survive to pass 2.
+__global__ void prune_kernel(const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ flags,
+                             const uint32_t* __restrict__ scan, const uint32_t* __restrict__ gsize,
+                             const uint64_t* __restrict__ bound, uint64_t threshold, uint64_t n,
+                             uint64_t* counts, uint32_t* surv, unsigned long long* pruned) {
+  const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t i = idx_sorted[j];
+  const uint32_t g = scan[j] + flags[j] - 1;
+  uint32_t s = 0;
+  if (gsize[g] == 1) {
+    counts[i] = bound[g];
+  } else if (bound[g] < threshold) {
+    counts[i] = kPrunedDev;
+    atomicAdd(pruned, 1ull);
+  } else {
+    counts[i] = 0;
+    s = 1;
+  }
+  surv[i] = s;
+}
+
+__global__ void gather_kernel(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
+                              uint64_t n, uint32_t L, const uint32_t* __restrict__ types,
+                              const uint32_t* __restrict__ win, const uint32_t* __restrict__ sigma,
+                              uint32_t* otypes, uint32_t* owin, uint32_t* osigma, uint32_t* oidx) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  const uint32_t o = scan[i];
+  for (uint32_t k = 0; k < L; ++k) otypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
+  for (uint32_t k = 0; k + 1 < L; ++k) owin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
+  osigma[o] = sigma[i];
+  oidx[o] = static_cast<uint32_t>(i);
+}
+
+__global__ void scatter_counts_kernel(const uint32_t* __restrict__ oidx, const uint64_t* __restrict__ c,
+                                      uint32_t m, uint64_t* counts) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o < m) counts[oidx[o]] = c[o];
+}
+
+__global__ void freq_flags_kernel(const uint64_t* __restrict__ counts, uint64_t threshold, uint64_t n,
+                                  uint32_t* flags) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t c = counts[i];
+  flags[i] = (c != kPrunedDev && c >= threshold) ? 1u : 0u;
+}
+
+__global__ void compact_freq_kernel(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
+                                    uint64_t n, uint32_t L, const uint32_t* __restrict__ types,
+                                    const uint32_t* __restrict__ win, const uint64_t* __restrict__ counts,
+                                    uint32_t* otypes, uint32_t* owin, uint64_t* ocounts) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || !flags[i]) return;
+  const uint32_t o = scan[i];
+  for (uint32_t k = 0; k < L; ++k) otypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
+  for (uint32_t k = 0; k + 1 < L; ++k) owin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
+  ocounts[o] = counts[i];
+}
+
+inline unsigned blocks_for(uint64_t n, unsigned t = 256) {
+  return static_cast<unsigned>((n + t - 1) / t);
+}
+
+}  // namespace
+
+// Exclusive scan of n u32 flags into scan[]; returns the total.
+uint32_t Engine::dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n) {
+  size_t tmp = 0;
+  EPI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flags, scan, static_cast<int>(n), st_));
+  void* d_tmp = scratch_.get<char>(kMCub, tmp + 16);
+  EPI_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, flags, scan, static_cast<int>(n), st_));
+  uint32_t last_scan = 0, last_flag = 0;
+  EPI_CUDA(cudaMemcpyAsync(&last_scan, scan + n - 1, 4, cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaMemcpyAsync(&last_flag, flags + n - 1, 4, cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaStreamSynchronize(st_));
+  return last_scan + last_flag;
+}
+
+// Counts of the device-resident candidate set `c` into d_counts: exact, or
+// two-pass (MINE) with PRUNED sentinels for eliminated candidates.
+void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
+                                   uint64_t* d_counts, epi_stats& stats) {
+  const uint64_t n = c.n;
+  const uint32_t L = c.N;
+  stats.episodes += n;
+  uint32_t bits = 1;
+  while ((1ull << bits) < stream_.alphabet + 1ull) ++bits;
+  const bool grouping = mode == EPI_MODE_MINE && threshold > 1 && L >= 2 && bits * L <= 64 &&
+                        n < (1ull << 31);
+  if (!grouping) {
+    stats.pass2_episodes += n;
+    count_device(c, d_counts, stats, &stats.pass2_ms);
+    return;
+  }
+  const uint32_t M = L - 1;
+  uint64_t* keys = scratch_.get<uint64_t>(kMKeys, n);
+  uint64_t* keys_alt = scratch_.get<uint64_t>(kMKeysAlt, n);
+  uint32_t* idx = scratch_.get<uint32_t>(kMIdx, n);
+  uint32_t* idx_alt = scratch_.get<uint32_t>(kMIdxAlt, n);
+  pack_keys_kernel<<<blocks_for(n), 256, 0, st_>>>(c.types, L, bits, n, keys, idx);
+  EPI_CUDA(cudaGetLastError());
+  cub::DoubleBuffer<uint64_t> kb(keys, keys_alt);
+  cub::DoubleBuffer<uint32_t> vb(idx, idx_alt);
+  size_t tmp = 0;
+  EPI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(n), 0,
+                                           static_cast<int>(bits * L), st_));
+  void* d_tmp = scratch_.get<char>(kMCub, tmp + 16);
+  EPI_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, kb, vb, static_cast<int>(n), 0,
+                                           static_cast<int>(bits * L), st_));
+  const uint64_t* skeys = kb.Current();
+  const uint32_t* sidx = vb.Current();
+  uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
+  uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
+  head_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(skeys, n, flags);
+  EPI_CUDA(cudaGetLastError());
+  const uint32_t n_groups = dev_exclusive_scan(flags, scan, n);
+  stats.kernel_launches += 4;
+
+  // group metadata + relaxed (hull) episodes
+  const size_t g_types = 0, g_win = align256(static_cast<size_t>(n_groups) * L * 4),
+               g_sigma = g_win + align256(static_cast<size_t>(n_groups) * M * 4),
+               g_start = g_sigma + align256(n_groups * 4ull), g_size = g_start + align256(n_groups * 4ull),
+               g_total = g_size + align256(n_groups * 4ull);
+  char* gbuf = scratch_.get<char>(kMGroups, g_total);
+  uint32_t* rtypes = reinterpret_cast<uint32_t*>(gbuf + g_types);
+  uint32_t* rwin = reinterpret_cast<uint32_t*>(gbuf + g_win);
+  uint32_t* rsigma = reinterpret_cast<uint32_t*>(gbuf + g_sigma);
+  uint32_t* gstart = reinterpret_cast<uint32_t*>(gbuf + g_start);
+  uint32_t* gsize = reinterpret_cast<uint32_t*>(gbuf + g_size);
+  group_starts_kernel<<<blocks_for(n), 256, 0, st_>>>(flags, scan, n, gstart);
+  hull_kernel<<<blocks_for(n_groups), 256, 0, st_>>>(c.types, c.win, L, sidx, gstart, n_groups, n,
+                                                     rtypes, rwin, rsigma, gsize);
+  EPI_CUDA(cudaGetLastError());
+  stats.kernel_launches += 2;
+  DevSet rel = c;
+  rel.n = n_groups;
+  rel.types = rtypes;
+  rel.win = rwin;
+  rel.sigma = rsigma;
+  rel.width = 0;  // hull widths differ in general
+  uint64_t* bound = scratch_.get<uint64_t>(kMGroupCnt, n_groups);
+  stats.pass1_groups += n_groups;
+  count_device(rel, bound, stats, &stats.pass1_ms);
+
+  // Survivor flags go to the index buffer the sort left free.
+  uint32_t* sflags = sidx == idx ? idx_alt : idx;
+  unsigned long long* d_pruned = reinterpret_cast<unsigned long long*>(scratch_.get<char>(kMPruned, 16));
+  EPI_CUDA(cudaMemsetAsync(d_pruned, 0, 8, st_));
+  prune_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx, flags, scan, gsize, bound, threshold, n,
+                                               d_counts, sflags, d_pruned);
+  EPI_CUDA(cudaGetLastError());
+  uint32_t* sscan = scan;
+  const uint32_t m = dev_exclusive_scan(sflags, sscan, n);
+  unsigned long long pruned = 0;
+  EPI_CUDA(cudaMemcpy(&pruned, d_pruned, 8, cudaMemcpyDeviceToHost));
+  stats.pruned += pruned;
+  stats.kernel_launches += 2;
+  stats.pass2_episodes += m;
+  if (m > 0) {
+    const size_t s_types = 0, s_win = align256(static_cast<size_t>(m) * L * 4),
+                 s_sigma = s_win + align256(static_cast<size_t>(m) * M * 4),
+                 s_idx = s_sigma + align256(m * 4ull), s_total = s_idx + align256(m * 4ull);
+    char* sbuf = scratch_.get<char>(kMSurv, s_total);
+    uint32_t* stypes = reinterpret_cast<uint32_t*>(sbuf + s_types);
+    uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
+    uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
+    uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
+    gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
+                                                  swin, ssigma, sidx_out);
+    EPI_CUDA(cudaGetLastError());
+    DevSet sv = c;
+    sv.n = m;
+    sv.types = stypes;
+    sv.win = swin;
+    sv.sigma = ssigma;
+    uint64_t* sc = scratch_.get<uint64_t>(kMSurvCnt, m);
+    count_device(sv, sc, stats, &stats.pass2_ms);
+    scatter_counts_kernel<<<blocks_for(m), 256, 0, st_>>>(sidx_out, sc, m, d_counts);
+    EPI_CUDA(cudaGetLastError());
+    stats.kernel_launches += 2;
+  }
+}
+
+// mine (E/miner.hpp:114-173), device-resident.
+void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
+  if (cfg.threshold < 1) throw Error(EPI_EINVAL, "mine: threshold must be >= 1");
+  if (cfg.max_level < 1) throw Error(EPI_EINVAL, "mine: max_level must be >= 1");
+  if (cfg.n_alpha == 0) throw Error(EPI_EINVAL, "mine: constraint alphabet must not be empty");
+  std::vector<uint32_t> awin(cfg.n_alpha), ahi(cfg.n_alpha);
+  int64_t amax = 0;
+  int awidth = -1;
+  for (uint64_t i = 0; i < cfg.n_alpha; ++i) {
+    const int64_t lo = cfg.alpha_low[i], hi = cfg.alpha_high[i];
+    if (lo < 0 || lo >= hi) throw Error(EPI_EINVAL, "interval constraint requires 0 <= low < high");
+    if (hi > kMaxHighWide)
+      throw Error(EPI_EUNSUPPORTED, "constraint high > 4095 ms is not supported by the device counter");
+    awin[i] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
+    ahi[i] = static_cast<uint32_t>(hi);
+    amax = std::max(amax, hi);
+    const int w = static_cast<int>(hi - lo);
+    awidth = awidth == -1 ? w : (awidth == w ? w : 0);
+  }
+  m_level_cands_.clear();
+  m_level_off_.assign(1, 0);
+  m_level_ms_.clear();
+  m_counts_.clear();
+  m_off_.assign(1, 0);
+  m_types_.clear();
+  m_lo_.clear();
+  m_hi_.clear();
+  epi_stats totals{};
+  const uint32_t A = stream_.alphabet;
+  const std::vector<uint64_t>& hist = stream_.type_hist;
+
+  // Frequent set of the previous level, host side (types, packed windows).
+  std::vector<uint32_t> ftypes, fwin;
+  uint32_t F = 0;
+  size_t nf = 0;
+
+  auto record_level = [&](size_t cands, uint32_t L, const uint32_t* t, const uint32_t* w,
+                          const uint64_t* cnt, size_t k, double ms) {
+    for (size_t i = 0; i < k; ++i) {
+      m_counts_.push_back(cnt[i]);
+      m_types_.insert(m_types_.end(), t + i * L, t + (i + 1) * L);
+      for (uint32_t j = 0; j + 1 < L; ++j) {
+        const uint32_t x = w[i * (L - 1) + j];
+        m_lo_.push_back(static_cast<int64_t>(x & 0xffff) - 1);
+        m_hi_.push_back(static_cast<int64_t>(x >> 16));
+      }
+      m_off_.push_back(static_cast<uint32_t>(m_types_.size()));
+    }
+    m_level_cands_.push_back(cands);
+    m_level_off_.push_back(m_counts_.size());
+    m_level_ms_.push_back(ms);
+  };
+
+  for (size_t level = 1; level <= cfg.max_level; ++level) {
+    auto t0 = std::chrono::steady_clock::now();
+    const uint32_t L = static_cast<uint32_t>(level);
+    if (level == 1) {
+      // Level 1: every type of the alphabet; counted on the host-set path.
+      EpisodeSet c1;
+      generate_candidates(1, EpisodeSet{}, {}, A, c1);
+      if (c1.size() == 0) break;
+      std::vector<uint64_t> counts;
+      count_set(c1, cfg.threshold, EPI_MODE_EXACT, counts, totals);
+      ftypes.clear();
+      std::vector<uint64_t> fc;
+      for (uint32_t t = 0; t < A; ++t)
+        if (counts[t] >= cfg.threshold) {
+          ftypes.push_back(t);
+          fc.push_back(counts[t]);
+        }
+      fwin.clear();
+      F = 1;
+      nf = ftypes.size();
+      record_level(A, 1, ftypes.data(), nullptr, fc.data(), nf,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      if (nf == 0) break;
+      continue;
+    }
+
+    // ---- candidate generation on the device ----------------------------
+    uint64_t n = 0;
+    uint64_t matched = 0;
+    std::vector<uint32_t> pre, lrange;
+    std::vector<uint64_t> loff;
+    if (level == 2) {
+      n = static_cast<uint64_t>(nf) * nf * cfg.n_alpha;
+      uint64_t hsum = 0;
+      for (uint32_t t : ftypes) hsum += hist[t];
+      matched = 2ull * cfg.n_alpha * nf * hsum;
+    } else {
+      // Join index over the frequent set: stable sort by the prefix key
+      // (first L-2 nodes + their constraints), exact comparisons.
+      const uint32_t K = F - 1;
+      auto cmp_key = [&](uint32_t a, uint32_t fa, uint32_t b, uint32_t fb) -> int {
+        for (uint32_t k = 0; k < K; ++k) {
+          const uint32_t x = ftypes[static_cast<size_t>(a) * F + fa + k],
+                         y = ftypes[static_cast<size_t>(b) * F + fb + k];
+          if (x != y) return x < y ? -1 : 1;
+        }
+        for (uint32_t k = 0; k + 1 < K; ++k) {
+          const uint32_t x = fwin[static_cast<size_t>(a) * (F - 1) + fa + k],
+                         y = fwin[static_cast<size_t>(b) * (F - 1) + fb + k];
+          if (x != y) return x < y ? -1 : 1;
+        }
+        return 0;
+      };
+      pre.resize(nf);
+      std::iota(pre.begin(), pre.end(), 0u);
+      std::stable_sort(pre.begin(), pre.end(),
+                       [&](uint32_t a, uint32_t b) { return cmp_key(a, 0, b, 0) < 0; });
+      // prefix sums of hist[last type] in sorted order (matched-pair stats)
+      std::vector<uint64_t> hlast(nf + 1, 0);
+      for (size_t b = 0; b < nf; ++b)
+        hlast[b + 1] = hlast[b] + hist[ftypes[static_cast<size_t>(pre[b]) * F + F - 1]];
+      lrange.resize(2 * nf);
+      loff.assign(nf + 1, 0);
+      for (uint32_t l = 0; l < nf; ++l) {
+        auto lo = std::lower_bound(pre.begin(), pre.end(), l, [&](uint32_t r, uint32_t left) {
+          return cmp_key(r, 0, left, 1) < 0;
+        });
+        auto hi = std::upper_bound(lo, pre.end(), l, [&](uint32_t left, uint32_t r) {
+          return cmp_key(left, 1, r, 0) < 0;
+        });
+        const uint32_t b0 = static_cast<uint32_t>(lo - pre.begin()), b1 = static_cast<uint32_t>(hi - pre.begin());
+        lrange[2 * l] = b0;
+        lrange[2 * l + 1] = b1;
+        loff[l + 1] = loff[l] + (b1 - b0);
+        uint64_t ml = 0;
+        for (uint32_t k = 0; k < F; ++k) ml += hist[ftypes[static_cast<size_t>(l) * F + k]];
+        matched += ml * (b1 - b0) + (hlast[b1] - hlast[b0]);
+      }
+      n = loff[nf];
+    }
+    if (n == 0) break;
+    if (n >= (1ull << 31)) throw Error(EPI_EUNSUPPORTED, "more than 2^31 candidates in one level");
+
+    uint32_t* d_types = scratch_.get<uint32_t>(kMTypes, n * L);
+    uint32_t* d_win = scratch_.get<uint32_t>(kMWin, n * (L - 1));
+    uint32_t* d_sigma = scratch_.get<uint32_t>(kMSigma, n);
+    uint64_t* d_counts = scratch_.get<uint64_t>(kMCounts, n);
+    if (level == 2) {
+      const size_t up = nf + 2 * cfg.n_alpha;
+      uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up * 4));
+      std::copy(ftypes.begin(), ftypes.end(), h);
+      std::copy(awin.begin(), awin.end(), h + nf);
+      std::copy(ahi.begin(), ahi.end(), h + nf + cfg.n_alpha);
+      uint32_t* d = scratch_.get<uint32_t>(kMFreq, up);
+      EPI_CUDA(cudaMemcpyAsync(d, h, up * 4, cudaMemcpyHostToDevice, st_));
+      totals.h2d_bytes += up * 4;
+      gen_level2_kernel<<<blocks_for(n), 256, 0, st_>>>(d, static_cast<uint32_t>(nf), d + nf,
+                                                        d + nf + cfg.n_alpha,
+                                                        static_cast<uint32_t>(cfg.n_alpha), d_types,
+                                                        d_win, d_sigma, n);
+      EPI_CUDA(cudaGetLastError());
+    } else {
+      // upload: frequent types/win/sigma + pre + lrange + loff
+      const size_t o_t = 0, o_w = align256(nf * F * 4), o_s = o_w + align256(nf * (F - 1) * 4),
+                   o_p = o_s + align256(nf * 4), o_r = o_p + align256(nf * 4),
+                   o_o = o_r + align256(nf * 8), o_end = o_o + align256((nf + 1) * 8);
+      char* h = static_cast<char*>(pin_up_.get(o_end));
+      std::memcpy(h + o_t, ftypes.data(), nf * F * 4);
+      std::memcpy(h + o_w, fwin.data(), nf * (F - 1) * 4);
+      uint32_t* hs = reinterpret_cast<uint32_t*>(h + o_s);
+      for (size_t i = 0; i < nf; ++i) {
+        uint32_t s = 0;
+        for (uint32_t k = 0; k + 1 < F; ++k) s += fwin[i * (F - 1) + k] >> 16;
+        hs[i] = s;
+      }
+      std::memcpy(h + o_p, pre.data(), nf * 4);
+      std::memcpy(h + o_r, lrange.data(), nf * 8);
+      std::memcpy(h + o_o, loff.data(), (nf + 1) * 8);
+      char* d = scratch_.get<char>(kMJoin, o_end);
+      EPI_CUDA(cudaMemcpyAsync(d, h, o_end, cudaMemcpyHostToDevice, st_));
+      totals.h2d_bytes += o_end;
+      const unsigned blocks = static_cast<unsigned>((nf * 32 + 255) / 256);
+      gen_join_kernel<<<blocks, 256, 0, st_>>>(
+          L, reinterpret_cast<const uint32_t*>(d + o_t), reinterpret_cast<const uint32_t*>(d + o_w),
+          reinterpret_cast<const uint32_t*>(d + o_s), static_cast<uint32_t>(nf),
+          reinterpret_cast<const uint32_t*>(d + o_p), reinterpret_cast<const uint32_t*>(d + o_r),
+          reinterpret_cast<const uint64_t*>(d + o_o), d_types, d_win, d_sigma);
+      EPI_CUDA(cudaGetLastError());
+    }
+    totals.kernel_launches += 1;
+
+    DevSet c;
+    c.N = L;
+    c.n = n;
+    c.types = d_types;
+    c.win = d_win;
+    c.sigma = d_sigma;
+    c.max_high = amax;
+    c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
+    c.width = awidth > 0 ? awidth : 0;
+    count_device_two_pass(c, cfg.threshold, cfg.mode, d_counts, totals);
+
+    // ---- threshold + compaction in candidate order ------------------------
+    uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
+    uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
+    freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(d_counts, cfg.threshold, n, flags);
+    EPI_CUDA(cudaGetLastError());
+    const uint32_t k = dev_exclusive_scan(flags, scan, n);
+    totals.kernel_launches += 2;
+    std::vector<uint32_t> ntypes(static_cast<size_t>(k) * L), nwin(static_cast<size_t>(k) * (L - 1));
+    std::vector<uint64_t> ncnt(k);
+    if (k > 0) {
+      const size_t o_t = 0, o_w = align256(static_cast<size_t>(k) * L * 4),
+                   o_c = o_w + align256(static_cast<size_t>(k) * (L - 1) * 4),
+                   o_end = o_c + align256(k * 8ull);
+      char* d = scratch_.get<char>(kMOut, o_end);
+      compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
+          flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(d + o_t),
+          reinterpret_cast<uint32_t*>(d + o_w), reinterpret_cast<uint64_t*>(d + o_c));
+      EPI_CUDA(cudaGetLastError());
+      char* h = static_cast<char*>(pin_down_.get(o_end));
+      EPI_CUDA(cudaMemcpyAsync(h, d, o_end, cudaMemcpyDeviceToHost, st_));
+      EPI_CUDA(cudaStreamSynchronize(st_));
+      totals.d2h_bytes += o_end;
+      totals.kernel_launches += 1;
+      std::memcpy(ntypes.data(), h + o_t, ntypes.size() * 4);
+      std::memcpy(nwin.data(), h + o_w, nwin.size() * 4);
+      std::memcpy(ncnt.data(), h + o_c, ncnt.size() * 8);
+    }
+    record_level(n, L, ntypes.data(), nwin.data(), ncnt.data(), k,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    ftypes.swap(ntypes);
+    fwin.swap(nwin);
+    F = L;
+    nf = k;
+    if (nf == 0) break;
+  }
+  out->n_levels = m_level_cands_.size();
+  out->level_candidates = m_level_cands_.data();
+  out->level_offsets = m_level_off_.data();
+  out->level_ms = m_level_ms_.data();
+  out->frequent.n_episodes = m_counts_.size();
+  out->frequent.offsets = m_off_.data();
+  out->frequent.types = m_types_.data();
+  out->frequent.low = m_lo_.data();
+  out->frequent.high = m_hi_.data();
+  out->counts = m_counts_.data();
+  out->totals = totals;
+}
+
+}  // namespace epi

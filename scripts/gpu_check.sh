@@ -1,10 +1,14 @@
+#!/bin/bash
+# One GPU round-trip: parity tests, the three single-GPU bench configs, a
+# launch list and one full ncu capture of the map kernel. Outputs land in
+# gpurun_out/ (merged back by gpurun).
 set -x
 mkdir -p gpurun_out
-cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu 2>&1 | tail -25 > gpurun_out/pytest_gpu3.log
+timeout 900 python -m pytest tests/ -q -m gpu -x 2>&1 | tail -25 > gpurun_out/pytest_gpu.log
 timeout 300 python bench.py --steps 5 --warmup 3 --cpu-seconds 5 > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
 timeout 300 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
 timeout 300 python bench.py --config cfg1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_cfg1.json 2> gpurun_out/bench_cfg1.err
+if [ "${NCU:-1}" = 1 ]; then
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:machines_kernel -s 2 -c 1 -o gpurun_out/prof_cfg3 python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_cfg3.log 2>&1
-tail -3 gpurun_out/ncu_cfg3.log
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:machines_kernel -s 2 -c 1 -o gpurun_out/prof_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_cfg3.log 2>&1
+fi

@@ -203,6 +203,35 @@ def test_cfg2_mining(ctx, golden_configs, mode):
         assert r.stats["pruned"] > 0
 
 
+@pytest.mark.parametrize("mode", [MODE_MINE, MODE_EXACT])
+def test_mine_known_answers(ctx, golden_kats, mode):
+    """T/test_miner.cpp mining cases (two-event stream, backend identity on
+    random_stream(rng(82)), apriori closure on rng(81)): CSV and per-level
+    candidate counts equal the reference's."""
+    from paper_0905_2203_b200 import EventStream, MiningConfig, mine, write_mining_csv
+    for k in golden_kats["mine"]:
+        types, times, a = stream_from_json(k)
+        s = EventStream(types, times, a)
+        cfg = MiningConfig(threshold=k["threshold"], constraint_alphabet=[tuple(b) for b in k["alphabet_bins"]],
+                           max_level=k["max_level"], mode=mode)
+        r = mine(s, cfg, ctx=ctx)
+        assert [lv.candidates for lv in r.levels] == k["level_candidates"], k["name"]
+        assert write_mining_csv(r) == k["csv"], k["name"]
+
+
+def test_mine_acceptance_c3(ctx):
+    """T/acceptance.cpp C3: four 9-node chains embedded at 1 Hz in 100 s of
+    64-neuron 20 Hz noise are all frequent at level 9 (threshold 50)."""
+    from paper_0905_2203_b200 import EventStream, MiningConfig, mine
+    chains = [Episode(list(range(9 * e, 9 * e + 9)), [(5, 10)] * 8) for e in range(4)]
+    types, times = generate_arrays(GenConfig(64, 100, 20, [Embedding(c, 1.0) for c in chains], 99177))
+    r = mine(EventStream(types, times, 64), MiningConfig(threshold=50, constraint_alphabet=[(5, 10)],
+                                                           max_level=9), ctx=ctx)
+    assert len(r.levels) >= 9 and r.levels[8].level == 9
+    found = {tuple(ep.types) for ep, _ in r.levels[8].frequent}
+    assert all(tuple(c.types) in found for c in chains)
+
+
 def test_cfg2_level3_bounds_sound(ctx, golden_configs):
     """Pass 1 never prunes a frequent candidate, and its bound is >= exact."""
     from paper_0905_2203_b200 import generate_candidates, Episode as E
