@@ -16,21 +16,39 @@ EPI_EXTERN_W(9) EPI_EXTERN_W(10) EPI_EXTERN_W(11) EPI_EXTERN_W(12)
 EPI_EXTERN_W(13) EPI_EXTERN_W(14) EPI_EXTERN_W(15) EPI_EXTERN_W(16)
 #undef EPI_EXTERN_W
 
-uint32_t chunk_tiles_for(uint32_t a_pad) {
-  uint32_t row = a_pad * 4u;
-  uint32_t ch = impl::kStageBytes / row;
-  return ch ? ch : 1u;
+int32_t stages_for(uint32_t blk_words) {
+  const uint32_t bytes = blk_words * 4u;
+  if (bytes <= 16u * 1024u) return 3;
+  if (bytes <= 48u * 1024u) return 2;
+  return 0;  // very large alphabets: rows read from global memory via L1
 }
 
-using NarrowAll =
-    impl::Dispatch<impl::NarrowW<0>::template H, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16>;
+// Generic (runtime-width) kernels: N 1..8 here, N 9..16 in count_g9.cu.
+using NarrowLo = impl::Dispatch<impl::NarrowW<0, false>::template H, 1, 2, 3, 4, 5, 6, 7, 8>;
+void launch_machines_generic_hi(int n_nodes, const CountLaunch& p, cudaStream_t st);
+void launch_walk_generic_hi(int n_nodes, const CountLaunch& p, cudaStream_t st);
 
-bool has_uniform_kernel(int n_nodes, int width) {
-  return n_nodes >= 2 && n_nodes <= 8 && width >= 1 && width <= 16;
+struct NarrowAll {
+  static void machines(int n, const CountLaunch& p, cudaStream_t st) {
+    if (n <= 8)
+      NarrowLo::machines(n, p, st);
+    else
+      launch_machines_generic_hi(n, p, st);
+  }
+  static void walk(int n, const CountLaunch& p, cudaStream_t st) {
+    if (n <= 8)
+      NarrowLo::walk(n, p, st);
+    else
+      launch_walk_generic_hi(n, p, st);
+  }
+};
+
+bool has_uniform_kernel(int n_nodes, int width, bool hi32) {
+  return hi32 && n_nodes >= 2 && n_nodes <= 8 && width >= 1 && width <= 16;
 }
 
-void launch_machines(int n_nodes, int width, const CountLaunch& p, cudaStream_t st) {
-  if (!has_uniform_kernel(n_nodes, width)) {
+void launch_machines(int n_nodes, int width, bool hi32, const CountLaunch& p, cudaStream_t st) {
+  if (!has_uniform_kernel(n_nodes, width, hi32)) {
     NarrowAll::machines(n_nodes, p, st);
     return;
   }

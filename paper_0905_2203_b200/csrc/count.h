@@ -8,15 +8,19 @@ namespace epi {
 
 // First completions recorded per FRESH machine for the concat-walk sync.
 constexpr int kRecorded = 4;
+// Bitmap layout: blocks of kBlkTiles tiles; per (block, type) a row of
+// kRowStride words (kBlkTiles tile words + 4 pad words for bank spread).
+constexpr int kBlkTiles = 32;
+constexpr uint32_t kRowStride = 36;
 
 struct CountLaunch {
-  const uint32_t* occ;     // tile-major type bitmaps (DeviceStream::d_occ)
-  uint32_t a_pad;          // words per tile row
+  const uint32_t* occ;     // blocked type bitmaps (DeviceStream::d_occ)
+  uint32_t blk_words;      // words per bitmap block (a_pad * kRowStride)
+  int32_t stages;          // shared-memory ring depth (0: read rows from global)
   int32_t n_tiles;
-  const int32_t* seg_g;    // P+1 segment tile bounds (device)
+  const int32_t* seg_g;    // P+1 segment tile bounds (device), multiples of 4
   int32_t P;               // segments
-  int32_t window_tiles;    // tiles staged before a segment for its window
-  int32_t chunk_tiles;     // tiles per shared-memory stage
+  int32_t window_tiles;    // tiles processed before a segment for its window
   int32_t hist_words;      // wide path: history words per position (ceil(max high / 32))
   uint32_t n_eps;          // episodes (all of length n_nodes)
   const uint32_t* ep_types;  // [n_eps * N]
@@ -26,13 +30,16 @@ struct CountLaunch {
   uint32_t* f_ncomp;         // [P * n_eps] FRESH completions incl. window
   uint64_t* f_last;          // [P * n_eps] last in-segment completion or ~0
   uint64_t* f_first;         // [P * n_eps * kRecorded] first completion times
-  uint64_t* counts;          // [n_eps] walk output
+  uint64_t* counts;          // [n_eps] walk output (map output when P == 1)
   unsigned long long* patches;  // walk statistics counter
+  int* occ_query;            // host: non-null -> launch_machines* reports CTAs/SM, no launch
 };
 
-uint32_t chunk_tiles_for(uint32_t a_pad);
-// width: launch-uniform window width high-low (0 = mixed) selects a specialised kernel.
-void launch_machines(int n_nodes, int width, const CountLaunch& p, cudaStream_t st);
+// Shared-memory ring depth for a bitmap block of blk_words words.
+int32_t stages_for(uint32_t blk_words);
+// width: launch-uniform window width high-low (0 = mixed); hi32: every
+// high <= 32. Together they select a specialised map kernel when available.
+void launch_machines(int n_nodes, int width, bool hi32, const CountLaunch& p, cudaStream_t st);
 void launch_walk(int n_nodes, const CountLaunch& p, cudaStream_t st);
 // high > 63 (up to kMaxHighWide): local-memory history ring.
 void launch_machines_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);

@@ -1,7 +1,7 @@
 // Exact non-overlapped episode counting on sm_100a: a bit-sliced counting
 // automaton, run segment-parallel (MapConcatenate) and stitched by a
-// per-episode concat walk. Included by count.cu (narrow windows, high <= 63)
-// and count_wide.cu (high <= 4095); see DESIGN.md.
+// per-episode concat walk. Included by count.cu / count_w*.cu (narrow
+// windows, high <= 63) and count_wide.cu (high <= 4095); see DESIGN.md.
 //
 // Semantics follow run_fsm / count_fsm (E/fsm.hpp:45-106) exactly:
 //   * an event of type tau at time t is admitted at position 0 iff t > pe
@@ -34,9 +34,15 @@
 // parallel and records its count, last completion and first kRecorded
 // completion times. The concat walk (one thread per episode) chains the
 // segments; when a boundary needs RESTART(L) it re-runs that machine inline
-// only until it completes at a time where the FRESH machine also completed -
-// from there both are identical, so the rest of the segment is read off the
+// only until it provably coincides with the FRESH machine (same completion,
+// or both quiet for sum(high)) and reads the rest of the segment off the
 // FRESH record ("patch", cf. E/mapconcat.hpp:144-148).
+//
+// Bitmap layout (DeviceStream): blocks of kBlkTiles = 32 tiles; inside a
+// block, type tau's 32 tile words are contiguous at tau * kRowStride
+// (kRowStride = 36: 4 pad words spread the rows over the shared-memory
+// banks). A lane fetches 4 consecutive tiles of its type with one 16-byte
+// load; a CTA stages one whole block (all types) per bulk copy.
 #pragma once
 
 #include "common.cuh"
@@ -47,7 +53,6 @@ namespace impl {
 
 constexpr int kMachThreads = 256;
 constexpr int kStages = 3;
-constexpr uint32_t kStageBytes = 8192;
 
 template <int N>
 struct EpParams {
@@ -73,6 +78,10 @@ __device__ __forceinline__ EpParams<N> load_episode(const CountLaunch& p, uint32
   return ep;
 }
 
+__device__ __forceinline__ size_t occ_index(int32_t g, uint32_t type, uint32_t blk_words) {
+  return static_cast<size_t>(g >> 5) * blk_words + type * kRowStride + (g & 31);
+}
+
 // ---- history policies -------------------------------------------------------
 
 // Window test over X = (c : h1 : h2) (96 bits, c the current tile): bit i of
@@ -80,17 +89,25 @@ __device__ __forceinline__ EpParams<N> load_episode(const CountLaunch& p, uint32
 // 32*g + i, i.e. at X index 64 + i - a. With Z = X >> (64 - hi) (64 bits,
 // Z[j] = X[64 - hi + j]) this is OR_{b < w} Z[i + b], w = hi - lo1 + 1:
 // two funnel shifts to extract Z, then a smear of width w. Branch-free;
-// requires w <= 32 (wider windows are split in two).
-template <int W>
+// requires w <= 32 (wider windows are split in two). kHi32: every high <= 32,
+// so X = (c : h1) and the selects disappear.
+template <int W, bool kHi32>
 __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
                                                uint32_t hi) {
-  const uint32_t s = 64u - hi;  // 1..63
-  const bool low = s < 32u;
-  const uint32_t w0 = low ? h2 : h1;
-  const uint32_t w1 = low ? h1 : c;
-  const uint32_t w2 = low ? c : 0u;
-  const uint32_t zl = __funnelshift_r(w0, w1, s & 31u);
-  const uint32_t zh = __funnelshift_r(w1, w2, s & 31u);
+  uint32_t zl, zh;
+  if constexpr (kHi32) {
+    const uint32_t s = 32u - hi;  // 0..31
+    zl = __funnelshift_r(h1, c, s);
+    zh = c >> s;
+  } else {
+    const uint32_t s = 64u - hi;  // 1..63
+    const bool low = s < 32u;
+    const uint32_t w0 = low ? h2 : h1;
+    const uint32_t w1 = low ? h1 : c;
+    const uint32_t w2 = low ? c : 0u;
+    zl = __funnelshift_r(w0, w1, s & 31u);
+    zh = __funnelshift_r(w1, w2, s & 31u);
+  }
   if constexpr (W > 0) {
     uint32_t d = zl;
 #pragma unroll
@@ -111,35 +128,37 @@ __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t
   }
 }
 
-// high <= 63: the entry bitmaps of the two previous tiles, in registers.
-// W > 0: every window of the launch has width high - low == W (compile-time
-// unrolled smear); W == 0: runtime widths.
-template <int N, int W = 0>
+// high <= 63: the entry bitmaps of the previous tiles, in registers (two
+// words; one when every high <= 32). W > 0: every window of the launch has
+// width high - low == W (compile-time unrolled smear); W == 0: runtime.
+template <int N, int W = 0, bool kHi32 = false>
 struct NarrowHist {
+  static constexpr bool kQuad = true;  // four tiles per 16-byte load, unrolled
   static constexpr int M = N > 1 ? N - 1 : 1;
+  static constexpr int M2 = kHi32 ? 1 : M;
   uint32_t h1[M];
-  uint32_t h2[M];
+  uint32_t h2[M2];
 
   __device__ __forceinline__ void reset(int32_t, int) {
 #pragma unroll
-    for (int k = 0; k < M; ++k) h1[k] = h2[k] = 0;
-  }
-  __device__ __forceinline__ void on_clear(int32_t) {
+    for (int k = 0; k < M; ++k) h1[k] = 0;
 #pragma unroll
-    for (int k = 0; k < M; ++k) h1[k] = h2[k] = 0;
+    for (int k = 0; k < M2; ++k) h2[k] = 0;
   }
+  __device__ __forceinline__ void on_clear(int32_t g) { reset(g, 0); }
   __device__ __forceinline__ static uint32_t dil(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
                                                  uint32_t hi) {
     if constexpr (W > 0) {
-      return window_any<W>(c, h1, h2, lo1, hi);
+      return window_any<W, kHi32>(c, h1, h2, lo1, hi);
     } else {
-      if (hi - lo1 < 32u) return window_any<0>(c, h1, h2, lo1, hi);
-      return window_any<0>(c, h1, h2, lo1, lo1 + 31u) | window_any<0>(c, h1, h2, lo1 + 32u, hi);
+      if (hi - lo1 < 32u) return window_any<0, kHi32>(c, h1, h2, lo1, hi);
+      return window_any<0, kHi32>(c, h1, h2, lo1, lo1 + 31u) |
+             window_any<0, kHi32>(c, h1, h2, lo1 + 32u, hi);
     }
   }
   __device__ __forceinline__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi,
                                              int32_t) const {
-    return dil(c, h1[k], h2[k], lo1, hi);
+    return dil(c, h1[k], kHi32 ? 0u : h2[kHi32 ? 0 : k], lo1, hi);
   }
   __device__ __forceinline__ static uint32_t dilate_fresh(uint32_t c, uint32_t lo1, uint32_t hi) {
     return dil(c, 0u, 0u, lo1, hi);
@@ -147,7 +166,7 @@ struct NarrowHist {
   __device__ __forceinline__ void push(const uint32_t* C, int32_t) {
 #pragma unroll
     for (int k = 0; k < N - 1; ++k) {
-      h2[k] = h1[k];
+      if constexpr (!kHi32) h2[k] = h1[k];
       h1[k] = C[k];
     }
   }
@@ -158,6 +177,7 @@ struct NarrowHist {
 // so a clear costs O(1).
 template <int N, int HWMAX>
 struct WideHist {
+  static constexpr bool kQuad = false;  // rare path: one tile per iteration, compact code
   static constexpr int M = N > 1 ? N - 1 : 1;
   static constexpr int kMask = HWMAX - 1;
   uint32_t ring[M][HWMAX];
@@ -258,12 +278,15 @@ struct Machine {
 };
 
 // Advance one tile. on_completion(time) returns true to stop the machine.
-template <int N, class Hist, class OnC>
+// kMask: the tile may lie at or before the position-0 threshold tile.
+template <int N, class Hist, bool kMask, class OnC>
 __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>& ep,
                                           const uint32_t (&occ)[N], int32_t g, OnC&& on_c) {
   uint32_t C[N];
   C[0] = occ[0];
-  if (g <= m.thr_tile) C[0] &= (g < m.thr_tile) ? 0u : m.thr_mask;
+  if constexpr (kMask) {
+    if (g <= m.thr_tile) C[0] &= (g < m.thr_tile) ? 0u : m.thr_mask;
+  }
 #pragma unroll
   for (int k = 1; k < N; ++k)
     C[k] = occ[k] & m.hist.dilate(k - 1, C[k - 1], ep.lo1[k - 1], ep.hi[k - 1], g);
@@ -287,25 +310,45 @@ __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>
   return false;
 }
 
-// Map step: FRESH machine of (episode, segment). Tiles of the segment (plus
-// its window) are staged through shared memory with bulk copies; every
-// thread of the CTA walks the same tiles, so one staged row serves all 256
-// episodes of the block.
+// Four consecutive tiles g..g+3 from 16-byte loads (v[k] = tiles of type k).
+template <int N, class Hist, bool kMask, class OnC>
+__device__ __forceinline__ void quad_step(Machine<N, Hist>& m, const EpParams<N>& ep,
+                                          const uint4 (&v)[N], int32_t g, OnC&& on_c) {
+  uint32_t o[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) o[k] = v[k].x;
+  tile_step<N, Hist, kMask>(m, ep, o, g, on_c);
+#pragma unroll
+  for (int k = 0; k < N; ++k) o[k] = v[k].y;
+  tile_step<N, Hist, kMask>(m, ep, o, g + 1, on_c);
+#pragma unroll
+  for (int k = 0; k < N; ++k) o[k] = v[k].z;
+  tile_step<N, Hist, kMask>(m, ep, o, g + 2, on_c);
+#pragma unroll
+  for (int k = 0; k < N; ++k) o[k] = v[k].w;
+  tile_step<N, Hist, kMask>(m, ep, o, g + 3, on_c);
+}
+
+// Map step: FRESH machine of (episode, segment). The CTA walks the bitmap
+// blocks covering its segment (plus window); with p.stages > 0 each block is
+// staged into shared memory by one bulk copy (TMA engine) in a ring of
+// p.stages buffers, otherwise (very large alphabets) lanes read their rows
+// from global memory through L1. Every thread of the CTA walks the same
+// tiles, so one staged block serves all 256 episodes of the block.
 template <int N, class Hist>
 __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunch p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   uint32_t* stage = reinterpret_cast<uint32_t*>(smem + 128);
-  const uint32_t a_pad = p.a_pad;
-  const uint32_t ch = static_cast<uint32_t>(p.chunk_tiles);
-  const uint32_t stage_words = ch * a_pad;
+  const uint32_t bw = p.blk_words;
+  const int stages = p.stages;
 
   const int q = blockIdx.y;
   const uint32_t e = blockIdx.x * kMachThreads + threadIdx.x;
   const bool active = e < p.n_eps;
   const int32_t gq = p.seg_g[q];
   const int32_t gend = p.seg_g[q + 1];
-  const int32_t g0 = gq - p.window_tiles > 0 ? gq - p.window_tiles : 0;
+  const int32_t g0 = (gq - p.window_tiles > 0 ? gq - p.window_tiles : 0) & ~3;
 
   EpParams<N> ep = load_episode<N>(p, active ? e : 0);
   Machine<N, Hist> m;
@@ -319,28 +362,30 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   uint64_t last = ~0ull;
   uint64_t* first = p.f_first + (static_cast<size_t>(q) * p.n_eps + e) * kRecorded;
 
-  const int32_t total_tiles = gend - g0;
-  const int32_t nchunks = (total_tiles + static_cast<int32_t>(ch) - 1) / static_cast<int32_t>(ch);
+  uint32_t row_off[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) row_off[k] = ep.type[k] * kRowStride;
+
+  const int32_t blk0 = g0 >> 5;
+  const int32_t nblk = ((gend - 1) >> 5) - blk0 + 1;
 
   auto issue = [&](int32_t c) {
-    const int32_t tg = g0 + c * static_cast<int32_t>(ch);
-    int32_t nt = gend - tg;
-    if (nt > static_cast<int32_t>(ch)) nt = static_cast<int32_t>(ch);
-    const uint32_t bytes = static_cast<uint32_t>(nt) * a_pad * 4u;
-    uint64_t* bar = &bars[c % kStages];
+    uint64_t* bar = &bars[c % stages];
     dev::fence_proxy_async();
-    dev::mbar_arrive_expect_tx(bar, bytes);
-    dev::bulk_g2s(stage + static_cast<size_t>(c % kStages) * stage_words,
-                  p.occ + static_cast<size_t>(tg) * a_pad, bytes, bar);
+    dev::mbar_arrive_expect_tx(bar, bw * 4u);
+    dev::bulk_g2s(stage + static_cast<size_t>(c % stages) * bw,
+                  p.occ + static_cast<size_t>(blk0 + c) * bw, bw * 4u, bar);
   };
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) dev::mbar_init(&bars[s], 1);
-    dev::fence_barrier_init();
+  if (stages > 0) {
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < stages; ++s) dev::mbar_init(&bars[s], 1);
+      dev::fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int32_t c = 0; c < stages - 1 && c < nblk; ++c) issue(c);
   }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int32_t c = 0; c < kStages - 1 && c < nchunks; ++c) issue(c);
 
   auto on_c = [&](uint64_t tc) -> bool {
     if (ncomp < kRecorded && active) first[ncomp] = tc;
@@ -352,28 +397,49 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
     return false;
   };
 
-  for (int32_t c = 0; c < nchunks; ++c) {
-    if (threadIdx.x == 0 && c + kStages - 1 < nchunks) issue(c + kStages - 1);
-    dev::mbar_wait(&bars[c % kStages], static_cast<uint32_t>(c / kStages) & 1u);
-    const uint32_t* buf = stage + static_cast<size_t>(c % kStages) * stage_words;
-    const int32_t tg = g0 + c * static_cast<int32_t>(ch);
-    int32_t nt = gend - tg;
-    if (nt > static_cast<int32_t>(ch)) nt = static_cast<int32_t>(ch);
-    for (int32_t t = 0; t < nt; ++t) {
-      const uint32_t* row = buf + static_cast<size_t>(t) * a_pad;
-      uint32_t occ[N];
-#pragma unroll
-      for (int k = 0; k < N; ++k) occ[k] = row[ep.type[k]];
-      tile_step<N, Hist>(m, ep, occ, tg + t, on_c);
+  for (int32_t c = 0; c < nblk; ++c) {
+    const uint32_t* buf;
+    if (stages > 0) {
+      if (threadIdx.x == 0 && c + stages - 1 < nblk) issue(c + stages - 1);
+      dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
+      buf = stage + static_cast<size_t>(c % stages) * bw;
+    } else {
+      buf = p.occ + static_cast<size_t>(blk0 + c) * bw;
     }
-    __syncthreads();
+    const int32_t gb = (blk0 + c) * 32;
+    const int32_t t0 = g0 > gb ? g0 - gb : 0;
+    const int32_t t1 = gend - gb < 32 ? gend - gb : 32;
+    if constexpr (Hist::kQuad) {
+      for (int32_t t = t0; t < t1; t += 4) {
+        uint4 v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = *reinterpret_cast<const uint4*>(buf + row_off[k] + t);
+        const int32_t g = gb + t;
+        if (g <= m.thr_tile)
+          quad_step<N, Hist, true>(m, ep, v, g, on_c);
+        else
+          quad_step<N, Hist, false>(m, ep, v, g, on_c);
+      }
+    } else {
+      for (int32_t t = t0; t < t1; ++t) {
+        uint32_t o[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) o[k] = buf[row_off[k] + t];
+        tile_step<N, Hist, true>(m, ep, o, gb + t, on_c);
+      }
+    }
+    if (stages > 0) __syncthreads();
   }
 
   if (active) {
-    const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
-    p.f_count[idx] = cnt;
-    p.f_ncomp[idx] = ncomp;
-    p.f_last[idx] = last;
+    if (p.P == 1) {
+      p.counts[e] = cnt;  // one segment from the stream start: exact, no walk
+    } else {
+      const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
+      p.f_count[idx] = cnt;
+      p.f_ncomp[idx] = ncomp;
+      p.f_last[idx] = last;
+    }
   }
 }
 
@@ -478,11 +544,10 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
           synced = true;
           break;
         }
-        const uint32_t* row = p.occ + static_cast<size_t>(g) * p.a_pad;
         uint32_t occ[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) occ[k] = __ldg(row + ep.type[k]);
-        if (tile_step<N, Hist>(m, ep, occ, g, on_c)) break;
+        for (int k = 0; k < N; ++k) occ[k] = __ldg(p.occ + occ_index(g, ep.type[k], p.blk_words));
+        if (tile_step<N, Hist, true>(m, ep, occ, g, on_c)) break;
       }
       if (!synced) {
         cnt = rc;
@@ -498,18 +563,34 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
   if (patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));
 }
 
+inline size_t machines_smem(const CountLaunch& p) {
+  return 128 + static_cast<size_t>(p.stages) * p.blk_words * 4;
+}
+
 template <int N, class Hist>
-void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
-  const uint32_t stage_words = static_cast<uint32_t>(p.chunk_tiles) * p.a_pad;
-  const size_t smem = 128 + static_cast<size_t>(kStages) * stage_words * 4;
+void configure_machines() {
   static bool configured = false;
   if (!configured) {
     EPI_CUDA(cudaFuncSetAttribute(machines_kernel<N, Hist>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured = true;
   }
+}
+
+// With p.occ_query set, report resident map CTAs per SM for this launch
+// shape (the segment planner's input) instead of launching.
+template <int N, class Hist>
+void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
+  configure_machines<N, Hist>();
+  if (p.occ_query) {
+    int blocks = 0;
+    EPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, machines_kernel<N, Hist>,
+                                                           kMachThreads, machines_smem(p)));
+    *p.occ_query = blocks > 0 ? blocks : 1;
+    return;
+  }
   dim3 grid((p.n_eps + kMachThreads - 1) / kMachThreads, p.P);
-  machines_kernel<N, Hist><<<grid, kMachThreads, smem, st>>>(p);
+  machines_kernel<N, Hist><<<grid, kMachThreads, machines_smem(p), st>>>(p);
   EPI_CUDA(cudaGetLastError());
 }
 
@@ -549,18 +630,17 @@ struct Dispatch<H, N, Rest...> {
   }
 };
 
-template <int W>
+template <int W, bool kHi32>
 struct NarrowW {
   template <int N>
-  using H = NarrowHist<N, W>;
+  using H = NarrowHist<N, W, kHi32>;
 };
 
-// Uniform-window-width map kernels (N 2..8), instantiated per W in
-// count_w*.cu so the compile parallelises.
+// Uniform-window-width map kernels (N 2..8, every high <= 32), instantiated
+// per W in count_w*.cu so the compile parallelises.
 template <int W>
 void launch_machines_w(int n, const CountLaunch& p, cudaStream_t st) {
-  Dispatch<NarrowW<W>::template H, 2, 3, 4, 5, 6, 7, 8>::machines(n, p, st);
+  Dispatch<NarrowW<W, true>::template H, 2, 3, 4, 5, 6, 7, 8>::machines(n, p, st);
 }
-
 }  // namespace impl
 }  // namespace epi

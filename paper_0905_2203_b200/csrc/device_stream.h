@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "count.h"
 
 namespace epi {
 
@@ -49,7 +50,8 @@ struct DeviceStream {
   uint64_t n_tiles = 0;    // 32 ms tiles covering the compressed span
   uint64_t span = 0;       // compressed time span (last compressed time + 1)
   uint32_t gap_cap = 64;   // gap compression cap of the current bitmap (> every high)
-  uint32_t* d_occ = nullptr;
+  uint32_t* d_occ = nullptr;  // blocked bitmaps, see count.h (kBlkTiles, kRowStride)
+  uint32_t blk_words = 0;     // words per bitmap block (a_pad * kRowStride)
   size_t occ_bytes = 0;
   uint32_t* d_types_raw = nullptr;  // validated SoA kept for bitmap rebuilds
   int64_t* d_times_raw = nullptr;

@@ -218,19 +218,53 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   if (wide) stream_.ensure_cap(ds.max_high, st_, scratch_);
   const int32_t hist_words = wide ? static_cast<int32_t>((ds.max_high + 31) / 32) : 2;
 
-  // MapConcatenate plan: enough (episode, segment) machines to fill the GPU,
-  // segments long enough that each window lies inside the previous segment.
+  CountLaunch p{};
+  p.occ = stream_.d_occ;
+  p.blk_words = stream_.blk_words;
+  p.stages = stages_for(stream_.blk_words);
+  p.hist_words = hist_words;
+  p.n_eps = static_cast<uint32_t>(n);
+  p.ep_types = ds.types;
+  p.ep_win = ds.win;
+  p.ep_sigma = ds.sigma;
+  p.counts = d_counts;
+  auto launch_map = [&]() {
+    if (wide)
+      launch_machines_wide(static_cast<int>(N), p, st_);
+    else
+      launch_machines(static_cast<int>(N), ds.width, ds.max_high <= 32, p, st_);
+  };
+
+  // MapConcatenate plan. Segments must each span sum(high) (the window of a
+  // segment lies inside its predecessor). Cost model in tile steps of one
+  // thread: waves(P) * (tiles/P + window) for the map kernel (waves = map
+  // CTAs over resident CTA slots) plus kWalkStep per segment for the
+  // sequential concat walk; P = 1 needs no walk at all.
   const int64_t n_tiles = static_cast<int64_t>(stream_.n_tiles);
+  const int64_t tiles4 = (n_tiles + 3) / 4 * 4;
   const uint32_t max_sigma = ds.max_sigma;
   const int32_t window_tiles = static_cast<int32_t>((max_sigma + 31) / 32 + 1);
-  // The concat walk is sequential in P, so P is capped (kMaxWalkSegments);
-  // segments of >= 32 tiles keep the window overhead and patch rate low.
   constexpr int64_t kMaxWalkSegments = 128;
+  constexpr double kWalkStep = 20.0;
+  int bps = 1;
+  p.occ_query = &bps;
+  launch_map();
+  p.occ_query = nullptr;
+  const int64_t slots = static_cast<int64_t>(num_sms_) * bps;
+  const int64_t ctas_x = (static_cast<int64_t>(n) + 255) / 256;
   const int64_t min_seg = std::max<int64_t>(window_tiles * 4, 32);
-  const int64_t target = static_cast<int64_t>(num_sms_) * 2048;
-  int64_t want = (target + static_cast<int64_t>(n) - 1) / static_cast<int64_t>(n);
-  int64_t max_p = std::max<int64_t>(1, n_tiles / min_seg);
-  int64_t P = std::clamp<int64_t>(want, 1, std::min<int64_t>(max_p, kMaxWalkSegments));
+  const int64_t max_p = std::clamp<int64_t>(tiles4 / min_seg, 1, kMaxWalkSegments);
+  int64_t P = 1;
+  double best = 1e300;
+  for (int64_t cand = 1; cand <= max_p; ++cand) {
+    const double waves = static_cast<double>((ctas_x * cand + slots - 1) / slots);
+    const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
+    const double cost = waves * per + (cand > 1 ? kWalkStep * cand : 0.0);
+    if (cost < best * 0.999) {
+      best = cost;
+      P = cand;
+    }
+  }
   if (const char* force = std::getenv("EPI_FORCE_SEGMENTS")) {
     // Test knob: many short segments exercise the concat walk on small
     // streams. Correctness only needs each segment to span sum(high).
@@ -238,11 +272,14 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     P = std::clamp<int64_t>(std::atoll(force), 1,
                             std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
   }
-  const int64_t seg_len = (n_tiles + P - 1) / P;
-  P = (n_tiles + seg_len - 1) / seg_len;
+  // Segment bounds are multiples of 4 tiles (the map kernel advances four
+  // tiles per 16-byte load); the last segment runs to the 4-aligned end (the
+  // bitmap is zero past the stream).
+  const int64_t seg_len = ((tiles4 + P - 1) / P + 3) / 4 * 4;
+  P = (tiles4 + seg_len - 1) / seg_len;
   int32_t* h_seg = static_cast<int32_t*>(pin_seg_.get((P + 1) * sizeof(int32_t)));
   for (int64_t q = 0; q < P; ++q) h_seg[q] = static_cast<int32_t>(q * seg_len);
-  h_seg[P] = static_cast<int32_t>(n_tiles);
+  h_seg[P] = static_cast<int32_t>(tiles4);
   int32_t* d_seg = scratch_.get<int32_t>(kSlotSegments, P + 1 + 6);
   EPI_CUDA(cudaMemcpyAsync(d_seg, h_seg, (P + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
   unsigned long long* d_patch = reinterpret_cast<unsigned long long*>(d_seg + ((P + 2) & ~1));
@@ -250,41 +287,29 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k).
   launch_matched_pairs(ds.types, n * N, stream_.d_hist, d_patch + 1, st_);
 
-  const size_t nm = static_cast<size_t>(P) * n;
+  const size_t nm = P > 1 ? static_cast<size_t>(P) * n : 1;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
                m_first = align_up(m_last + nm * 8, 256), m_total = m_first + nm * 8 * kRecorded;
   char* d_mach = scratch_.get<char>(kSlotMachines, m_total);
-
-  CountLaunch p{};
-  p.occ = stream_.d_occ;
-  p.a_pad = stream_.a_pad;
   p.n_tiles = static_cast<int32_t>(n_tiles);
   p.seg_g = d_seg;
   p.P = static_cast<int32_t>(P);
   p.window_tiles = window_tiles;
-  p.chunk_tiles = static_cast<int32_t>(chunk_tiles_for(stream_.a_pad));
-  p.hist_words = hist_words;
-  p.n_eps = static_cast<uint32_t>(n);
-  p.ep_types = ds.types;
-  p.ep_win = ds.win;
-  p.ep_sigma = ds.sigma;
   p.f_count = reinterpret_cast<uint32_t*>(d_mach + m_count);
   p.f_ncomp = reinterpret_cast<uint32_t*>(d_mach + m_ncomp);
   p.f_last = reinterpret_cast<uint64_t*>(d_mach + m_last);
   p.f_first = reinterpret_cast<uint64_t*>(d_mach + m_first);
-  p.counts = d_counts;
   p.patches = d_patch;
 
   EPI_CUDA(cudaEventRecord(ev0_, st_));
-  if (wide)
-    launch_machines_wide(static_cast<int>(N), p, st_);
-  else
-    launch_machines(static_cast<int>(N), ds.width, p, st_);
+  launch_map();
   EPI_CUDA(cudaEventRecord(ev2_, st_));
-  if (wide)
-    launch_walk_wide(static_cast<int>(N), p, st_);
-  else
-    launch_walk(static_cast<int>(N), p, st_);
+  if (P > 1) {
+    if (wide)
+      launch_walk_wide(static_cast<int>(N), p, st_);
+    else
+      launch_walk(static_cast<int>(N), p, st_);
+  }
   EPI_CUDA(cudaEventRecord(ev1_, st_));
   unsigned long long h_patch[2] = {0, 0};
   EPI_CUDA(cudaMemcpyAsync(h_patch, d_patch, sizeof h_patch, cudaMemcpyDeviceToHost, st_));
@@ -294,7 +319,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   EPI_CUDA(cudaEventElapsedTime(&map_ms, ev0_, ev2_));
   stats.patches += h_patch[0];
   stats.segments = static_cast<uint64_t>(P);
-  stats.kernel_launches += 2;
+  stats.kernel_launches += P > 1 ? 3 : 2;  // matched-pair stats + map (+ walk)
   stats.map_launches += 1;
   stats.total_ms += ms;
   stats.map_ms += map_ms;

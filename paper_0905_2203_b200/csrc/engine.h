@@ -86,8 +86,9 @@ class Engine {
   void count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                    double* ms_out);
   void count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out);
-  void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode, uint64_t* d_counts,
-                             epi_stats& stats);
+  // uniform_win != 0: pass-1 relaxation uses that window at every position.
+  void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
+                             uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats);
   uint32_t dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n);
   void h2d(void* dst, const void* src, size_t bytes);
 

@@ -128,9 +128,10 @@ __global__ void __launch_bounds__(kLoadThreads)
     uint64_t i = base + j;
     c += gaps[j];
     if (i < n) {
-      uint64_t g = c >> 5;
+      const uint64_t g = c >> 5;
       const uint32_t ty = types[i];
-      atomicOr(&occ[g * a_pad + ty], 1u << (c & 31));
+      // blocked layout: block g/32, row `ty` (kRowStride words), word g%32
+      atomicOr(&occ[(g >> 5) * (a_pad * kRowStride) + ty * kRowStride + (g & 31)], 1u << (c & 31));
       if (smem_hist)
         atomicAdd(&s_hist[ty], 1u);
       else
@@ -243,8 +244,11 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
 }
 
 void DeviceStream::ensure_occ(uint64_t tiles, cudaStream_t st) {
-  // Pad the allocation so staged chunk reads never run past the end.
-  const size_t need = (tiles + 1) * static_cast<size_t>(a_pad) * sizeof(uint32_t);
+  // Whole blocks of kBlkTiles tiles plus one spare block, zero-filled: the
+  // map kernel may run up to the end of the last block.
+  blk_words = a_pad * kRowStride;
+  const size_t blocks = (tiles + kBlkTiles - 1) / kBlkTiles + 1;
+  const size_t need = blocks * blk_words * sizeof(uint32_t);
   if (need > occ_bytes) {
     if (d_occ) cudaFree(d_occ);
     d_occ = nullptr;

@@ -122,11 +122,16 @@ __global__ void group_starts_kernel(const uint32_t* __restrict__ flags,
   if (flags[j]) gstart[scan[j]] = static_cast<uint32_t>(j);
 }
 
-// One thread per group: hull of the members' windows.
+// One thread per group: the relaxed episode of the group. With
+// uniform_win != 0 every constraint becomes that window (the hull of the
+// whole constraint alphabet: contains every member's window, so still a sound
+// bound, and launch-uniform, so pass 1 runs on the width-specialised
+// kernels); otherwise the per-position hull of the members' windows.
 __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* __restrict__ win,
                             uint32_t L, const uint32_t* __restrict__ idx_sorted,
                             const uint32_t* __restrict__ gstart, uint32_t n_groups, uint64_t n,
-                            uint32_t* rtypes, uint32_t* rwin, uint32_t* rsigma, uint32_t* gsize) {
+                            uint32_t uniform_win, uint32_t* rtypes, uint32_t* rwin,
+                            uint32_t* rsigma, uint32_t* gsize) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_groups) return;
   const uint32_t j0 = gstart[g];
@@ -137,10 +142,15 @@ __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* 
   uint32_t sig = 0;
   for (uint32_t k = 0; k < M; ++k) {
     uint32_t lo1 = 0xffffu, hi = 0;
-    for (uint32_t j = j0; j < j1; ++j) {
-      const uint32_t w = win[static_cast<size_t>(idx_sorted[j]) * M + k];
-      lo1 = min(lo1, w & 0xffffu);
-      hi = max(hi, w >> 16);
+    if (uniform_win) {
+      lo1 = uniform_win & 0xffffu;
+      hi = uniform_win >> 16;
+    } else {
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint32_t w = win[static_cast<size_t>(idx_sorted[j]) * M + k];
+        lo1 = min(lo1, w & 0xffffu);
+        hi = max(hi, w >> 16);
+      }
     }
     rwin[static_cast<size_t>(g) * M + k] = lo1 | (hi << 16);
     sig += hi;
@@ -149,18 +159,19 @@ __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* 
   gsize[g] = j1 - j0;
 }
 
-// Per sorted position: singleton groups are exact, bound < threshold prunes,
-// the rest survive to pass 2.
+// Per sorted position: bound < threshold prunes, the rest survive to pass 2
+// (singleton groups are final when their relaxation is the episode itself).
 __global__ void prune_kernel(const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ flags,
                              const uint32_t* __restrict__ scan, const uint32_t* __restrict__ gsize,
                              const uint64_t* __restrict__ bound, uint64_t threshold, uint64_t n,
-                             uint64_t* counts, uint32_t* surv, unsigned long long* pruned) {
+                             bool singletons_exact, uint64_t* counts, uint32_t* surv,
+                             unsigned long long* pruned) {
   const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const uint32_t i = idx_sorted[j];
   const uint32_t g = scan[j] + flags[j] - 1;
   uint32_t s = 0;
-  if (gsize[g] == 1) {
+  if (singletons_exact && gsize[g] == 1) {
     counts[i] = bound[g];
   } else if (bound[g] < threshold) {
     counts[i] = kPrunedDev;
@@ -233,7 +244,7 @@ uint32_t Engine::dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint6
 // Counts of the device-resident candidate set `c` into d_counts: exact, or
 // two-pass (MINE) with PRUNED sentinels for eliminated candidates.
 void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
-                                   uint64_t* d_counts, epi_stats& stats) {
+                                   uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats) {
   const uint64_t n = c.n;
   const uint32_t L = c.N;
   stats.episodes += n;
@@ -283,7 +294,7 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   uint32_t* gsize = reinterpret_cast<uint32_t*>(gbuf + g_size);
   group_starts_kernel<<<blocks_for(n), 256, 0, st_>>>(flags, scan, n, gstart);
   hull_kernel<<<blocks_for(n_groups), 256, 0, st_>>>(c.types, c.win, L, sidx, gstart, n_groups, n,
-                                                     rtypes, rwin, rsigma, gsize);
+                                                     uniform_win, rtypes, rwin, rsigma, gsize);
   EPI_CUDA(cudaGetLastError());
   stats.kernel_launches += 2;
   DevSet rel = c;
@@ -291,7 +302,9 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   rel.types = rtypes;
   rel.win = rwin;
   rel.sigma = rsigma;
-  rel.width = 0;  // hull widths differ in general
+  // per-group hull widths differ in general; the alphabet hull is uniform
+  rel.width = uniform_win ? static_cast<int>((uniform_win >> 16) - (uniform_win & 0xffffu) + 1) : 0;
+  if (uniform_win) rel.max_sigma = (uniform_win >> 16) * (L - 1);
   uint64_t* bound = scratch_.get<uint64_t>(kMGroupCnt, n_groups);
   stats.pass1_groups += n_groups;
   count_device(rel, bound, stats, &stats.pass1_ms);
@@ -300,8 +313,10 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   uint32_t* sflags = sidx == idx ? idx_alt : idx;
   unsigned long long* d_pruned = reinterpret_cast<unsigned long long*>(scratch_.get<char>(kMPruned, 16));
   EPI_CUDA(cudaMemsetAsync(d_pruned, 0, 8, st_));
+  // A singleton group's per-group hull is the episode itself (exact); the
+  // uniform alphabet hull is only a bound.
   prune_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx, flags, scan, gsize, bound, threshold, n,
-                                               d_counts, sflags, d_pruned);
+                                               uniform_win == 0, d_counts, sflags, d_pruned);
   EPI_CUDA(cudaGetLastError());
   uint32_t* sscan = scan;
   const uint32_t m = dev_exclusive_scan(sflags, sscan, n);
@@ -341,7 +356,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
   if (cfg.max_level < 1) throw Error(EPI_EINVAL, "mine: max_level must be >= 1");
   if (cfg.n_alpha == 0) throw Error(EPI_EINVAL, "mine: constraint alphabet must not be empty");
   std::vector<uint32_t> awin(cfg.n_alpha), ahi(cfg.n_alpha);
-  int64_t amax = 0;
+  int64_t amax = 0, amin_lo = INT64_MAX;
   int awidth = -1;
   for (uint64_t i = 0; i < cfg.n_alpha; ++i) {
     const int64_t lo = cfg.alpha_low[i], hi = cfg.alpha_high[i];
@@ -351,9 +366,12 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
     awin[i] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
     ahi[i] = static_cast<uint32_t>(hi);
     amax = std::max(amax, hi);
+    amin_lo = std::min(amin_lo, lo);
     const int w = static_cast<int>(hi - lo);
     awidth = awidth == -1 ? w : (awidth == w ? w : 0);
   }
+  // Pass-1 relaxation window: the hull (min low, max high] of the alphabet.
+  const uint32_t alpha_hull = static_cast<uint32_t>(amin_lo + 1) | (static_cast<uint32_t>(amax) << 16);
   m_level_cands_.clear();
   m_level_off_.assign(1, 0);
   m_level_ms_.clear();
@@ -528,7 +546,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
     c.max_high = amax;
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
-    count_device_two_pass(c, cfg.threshold, cfg.mode, d_counts, totals);
+    count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, d_counts, totals);
 
     // ---- threshold + compaction in candidate order ------------------------
     uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);

@@ -219,6 +219,29 @@ def test_mine_known_answers(ctx, golden_kats, mode):
         assert write_mining_csv(r) == k["csv"], k["name"]
 
 
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference build (oracle/_ref) absent")
+@pytest.mark.parametrize("seed", range(4))
+def test_mine_random_vs_reference(ctx, seed):
+    """Device-resident mining (both modes) == the reference's mine() run
+    live (oracle/_ref) on random bursty streams: per-level candidate counts
+    and the full CSV (episodes, order, counts)."""
+    from paper_0905_2203_b200 import EventStream, MiningConfig, mine, write_mining_csv
+    rng = np.random.default_rng(900 + seed)
+    a = int(rng.integers(3, 9))
+    n = int(rng.integers(2000, 6000))
+    times = np.cumsum(rng.integers(0, [2, 4, 8, 16][seed] + 1, n)).astype(np.int64)
+    types = rng.integers(0, a, n).astype(np.uint32)
+    bins = [[(0, 5), (5, 10), (10, 15)], [(0, 4), (2, 7)], [(1, 9)], [(0, 3), (3, 6), (6, 9), (9, 12)]][seed]
+    thr = int(max(2, n // (a * a * 4)))
+    csv_ref, cands_ref, _ = oracle.ref_mine(types, times, a, thr, bins, 5, switch_level=99, backend=0,
+                                            workers=4)
+    s = EventStream(types, times, a)
+    for mode in (MODE_MINE, MODE_EXACT):
+        r = mine(s, MiningConfig(threshold=thr, constraint_alphabet=bins, max_level=5, mode=mode), ctx=ctx)
+        assert [lv.candidates for lv in r.levels] == cands_ref, (seed, mode)
+        assert write_mining_csv(r) == csv_ref, (seed, mode)
+
+
 def test_mine_acceptance_c3(ctx):
     """T/acceptance.cpp C3: four 9-node chains embedded at 1 Hz in 100 s of
     64-neuron 20 Hz noise are all frequent at level 9 (threshold 50)."""
