@@ -95,7 +95,15 @@ template <int W, bool kHi32>
 __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
                                                uint32_t hi) {
   uint32_t zl, zh;
-  if constexpr (kHi32) {
+  if constexpr (kHi32 && W > 0) {
+    // X = (c : h1); term b of the smear is (c : h1) >> (32 - hi + b), and
+    // 32 - hi + b <= 32 - lo1 <= 31, so each term is one funnel shift.
+    const uint32_t s = 32u - hi;
+    uint32_t d = __funnelshift_r(h1, c, s);
+#pragma unroll
+    for (int b = 1; b < W; ++b) d |= __funnelshift_r(h1, c, s + b);
+    return d;
+  } else if constexpr (kHi32) {
     const uint32_t s = 32u - hi;  // 0..31
     zl = __funnelshift_r(h1, c, s);
     zh = c >> s;
@@ -311,6 +319,9 @@ __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>
 }
 
 // Four consecutive tiles g..g+3 from 16-byte loads (v[k] = tiles of type k).
+// (A speculative no-completion fast path per quad was measured slower: with
+// 32 episodes per warp about half of all quads hold some lane's completion,
+// so the warp replays the quad anyway.)
 template <int N, class Hist, bool kMask, class OnC>
 __device__ __forceinline__ void quad_step(Machine<N, Hist>& m, const EpParams<N>& ep,
                                           const uint4 (&v)[N], int32_t g, OnC&& on_c) {
@@ -397,23 +408,14 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
     return false;
   };
 
-  for (int32_t c = 0; c < nblk; ++c) {
-    const uint32_t* buf;
-    if (stages > 0) {
-      if (threadIdx.x == 0 && c + stages - 1 < nblk) issue(c + stages - 1);
-      dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
-      buf = stage + static_cast<size_t>(c % stages) * bw;
-    } else {
-      buf = p.occ + static_cast<size_t>(blk0 + c) * bw;
-    }
-    const int32_t gb = (blk0 + c) * 32;
-    const int32_t t0 = g0 > gb ? g0 - gb : 0;
-    const int32_t t1 = gend - gb < 32 ? gend - gb : 32;
+  // One bitmap block: tiles [t0, t1) of block starting at tile gb, rows read
+  // through `rd(k, t)` (shared-memory or global flavour).
+  auto run_block = [&](int32_t gb, int32_t t0, int32_t t1, auto&& rd4, auto&& rd1) {
     if constexpr (Hist::kQuad) {
       for (int32_t t = t0; t < t1; t += 4) {
         uint4 v[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = *reinterpret_cast<const uint4*>(buf + row_off[k] + t);
+        for (int k = 0; k < N; ++k) v[k] = rd4(k, t);
         const int32_t g = gb + t;
         if (g <= m.thr_tile)
           quad_step<N, Hist, true>(m, ep, v, g, on_c);
@@ -424,11 +426,33 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
       for (int32_t t = t0; t < t1; ++t) {
         uint32_t o[N];
 #pragma unroll
-        for (int k = 0; k < N; ++k) o[k] = buf[row_off[k] + t];
+        for (int k = 0; k < N; ++k) o[k] = rd1(k, t);
         tile_step<N, Hist, true>(m, ep, o, gb + t, on_c);
       }
     }
-    if (stages > 0) __syncthreads();
+  };
+
+  for (int32_t c = 0; c < nblk; ++c) {
+    const int32_t gb = (blk0 + c) * 32;
+    const int32_t t0 = g0 > gb ? g0 - gb : 0;
+    const int32_t t1 = gend - gb < 32 ? gend - gb : 32;
+    if (stages > 0) {
+      if (threadIdx.x == 0 && c + stages - 1 < nblk) issue(c + stages - 1);
+      dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
+      // index the extern __shared__ array directly so the loads are LDS
+      const uint32_t sbase = static_cast<uint32_t>(c % stages) * bw;
+      run_block(
+          gb, t0, t1,
+          [&](int k, int32_t t) { return *reinterpret_cast<const uint4*>(&stage[sbase + row_off[k] + t]); },
+          [&](int k, int32_t t) { return stage[sbase + row_off[k] + t]; });
+      __syncthreads();
+    } else {
+      const uint32_t* gbuf = p.occ + static_cast<size_t>(blk0 + c) * bw;
+      run_block(
+          gb, t0, t1,
+          [&](int k, int32_t t) { return __ldg(reinterpret_cast<const uint4*>(gbuf + row_off[k] + t)); },
+          [&](int k, int32_t t) { return __ldg(gbuf + row_off[k] + t); });
+    }
   }
 
   if (active) {
