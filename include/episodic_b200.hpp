@@ -57,22 +57,20 @@ class Context {
   Context& operator=(const Context&) = delete;
   epi_ctx* get() const { return ctx_; }
 
+  // (Re)loads the stream on every call: an address/size cache would be
+  // fooled by a new stream constructed where an old one lived. Callers that
+  // count many batches over one stream use count_batch / mine.
   template <class Stream, class DataErrorT = std::runtime_error>
   void load(const Stream& s) {
-    if (loaded_ == static_cast<const void*>(&s) && loaded_n_ == s.size()) return;
     std::vector<uint32_t> types(s.types().begin(), s.types().end());
     std::vector<int64_t> times(s.times().begin(), s.times().end());
     throw_status<DataErrorT>(
         epi_load_stream(ctx_, types.data(), times.data(), types.size(), s.alphabet_size()),
         epi_last_error(ctx_));
-    loaded_ = &s;
-    loaded_n_ = s.size();
   }
 
  private:
   epi_ctx* ctx_ = nullptr;
-  const void* loaded_ = nullptr;
-  size_t loaded_n_ = 0;
 };
 
 // CSR form of a range of reference-shaped episodes (epi_episode_batch).

@@ -85,6 +85,38 @@ __global__ void matched_pairs_kernel(const uint32_t* __restrict__ types, uint64_
 }
 }  // namespace
 
+namespace {
+// Single-node episodes: every distinct firing time of the type is one
+// completion (pe = t, and the next time is > t), so the count is the
+// popcount of the type's bitmap rows. One thread per (episode, block).
+__global__ void singletons_kernel(const uint32_t* __restrict__ occ, uint32_t blk_words,
+                                  uint32_t n_blocks, const uint32_t* __restrict__ types,
+                                  uint32_t n_eps, unsigned long long* counts) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<uint64_t>(n_eps) * n_blocks) return;
+  const uint32_t e = static_cast<uint32_t>(i / n_blocks), b = static_cast<uint32_t>(i % n_blocks);
+  const uint4* row = reinterpret_cast<const uint4*>(occ + static_cast<size_t>(b) * blk_words +
+                                                    types[e] * kRowStride);
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kBlkTiles / 4; ++j) {
+    const uint4 v = __ldg(row + j);
+    c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+  }
+  if (c) atomicAdd(counts + e, static_cast<unsigned long long>(c));
+}
+}  // namespace
+
+void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_blocks,
+                       const uint32_t* types, uint32_t n_eps, uint64_t* counts, cudaStream_t st) {
+  EPI_CUDA(cudaMemsetAsync(counts, 0, static_cast<size_t>(n_eps) * sizeof(uint64_t), st));
+  const uint64_t threads = static_cast<uint64_t>(n_eps) * n_blocks;
+  if (threads == 0) return;
+  singletons_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      occ, blk_words, n_blocks, types, n_eps, reinterpret_cast<unsigned long long*>(counts));
+  EPI_CUDA(cudaGetLastError());
+}
+
 void launch_matched_pairs(const uint32_t* types, uint64_t count, const unsigned long long* hist,
                           unsigned long long* out, cudaStream_t st) {
   if (count == 0 || hist == nullptr) return;

@@ -44,6 +44,9 @@ void launch_walk(int n_nodes, const CountLaunch& p, cudaStream_t st);
 // high > 63 (up to kMaxHighWide): local-memory history ring.
 void launch_machines_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
+// Exact counts of single-node episodes (popcount of the type's bitmap).
+void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_blocks,
+                       const uint32_t* types, uint32_t n_eps, uint64_t* counts, cudaStream_t st);
 // *out += sum_i hist[types[i]] (matched-pair work model of a launch).
 void launch_matched_pairs(const uint32_t* types, uint64_t count, const unsigned long long* hist,
                           unsigned long long* out, cudaStream_t st);

@@ -212,6 +212,25 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const size_t n = ds.n;
   if (n == 0) return;
   const uint32_t N = ds.N;
+  if (N == 1) {
+    // every distinct firing time is a completion: popcount of the bitmap
+    const uint32_t n_blocks = static_cast<uint32_t>((stream_.n_tiles + kBlkTiles - 1) / kBlkTiles);
+    EPI_CUDA(cudaEventRecord(ev0_, st_));
+    launch_singletons(stream_.d_occ, stream_.blk_words, n_blocks, ds.types, static_cast<uint32_t>(n),
+                      d_counts, st_);
+    EPI_CUDA(cudaEventRecord(ev1_, st_));
+    EPI_CUDA(cudaEventSynchronize(ev1_));
+    float ms = 0;
+    EPI_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    stats.kernel_launches += 1;
+    stats.map_launches += 1;
+    stats.total_ms += ms;
+    stats.map_ms += ms;
+    stats.episode_events += static_cast<uint64_t>(n) * stream_.n;
+    stats.tile_steps += static_cast<uint64_t>(n) * n_blocks * kBlkTiles;
+    if (ms_out) *ms_out += ms;
+    return;
+  }
   // Wide windows need a bitmap whose gap compression cap exceeds them, and
   // the local-memory history ring (hist_words 32 ms words per position).
   const bool wide = ds.max_high > kMaxHigh;
@@ -311,8 +330,9 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
       launch_walk(static_cast<int>(N), p, st_);
   }
   EPI_CUDA(cudaEventRecord(ev1_, st_));
-  unsigned long long h_patch[2] = {0, 0};
-  EPI_CUDA(cudaMemcpyAsync(h_patch, d_patch, sizeof h_patch, cudaMemcpyDeviceToHost, st_));
+  unsigned long long* h_patch = static_cast<unsigned long long*>(pin_small_.get(64)) + 4;
+  EPI_CUDA(cudaMemcpyAsync(h_patch, d_patch, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           st_));
   EPI_CUDA(cudaStreamSynchronize(st_));
   float ms = 0, map_ms = 0;
   EPI_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));

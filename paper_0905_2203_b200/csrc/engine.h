@@ -89,7 +89,9 @@ class Engine {
   // uniform_win != 0: pass-1 relaxation uses that window at every position.
   void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
                              uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats);
-  uint32_t dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n);
+  uint32_t dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n,
+                              const unsigned long long* extra = nullptr,
+                              unsigned long long* extra_out = nullptr);
   void h2d(void* dst, const void* src, size_t bytes);
 
   int device_;
@@ -98,7 +100,7 @@ class Engine {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, ev2_ = nullptr;
   DeviceStream stream_;
   DeviceScratch scratch_;
-  PinnedBuffer pin_up_, pin_down_, pin_seg_;
+  PinnedBuffer pin_up_, pin_down_, pin_seg_, pin_small_;
 
   // epi_mine result storage
   std::vector<uint64_t> m_level_cands_, m_level_off_, m_counts_;

@@ -229,16 +229,20 @@ inline unsigned blocks_for(uint64_t n, unsigned t = 256) {
 }  // namespace
 
 // Exclusive scan of n u32 flags into scan[]; returns the total.
-uint32_t Engine::dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n) {
+// One stream sync returns the total (and, optionally, one more device u64).
+uint32_t Engine::dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n,
+                                    const unsigned long long* extra, unsigned long long* extra_out) {
   size_t tmp = 0;
   EPI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flags, scan, static_cast<int>(n), st_));
   void* d_tmp = scratch_.get<char>(kMCub, tmp + 16);
   EPI_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, flags, scan, static_cast<int>(n), st_));
-  uint32_t last_scan = 0, last_flag = 0;
-  EPI_CUDA(cudaMemcpyAsync(&last_scan, scan + n - 1, 4, cudaMemcpyDeviceToHost, st_));
-  EPI_CUDA(cudaMemcpyAsync(&last_flag, flags + n - 1, 4, cudaMemcpyDeviceToHost, st_));
+  uint32_t* h = static_cast<uint32_t*>(pin_small_.get(32));
+  EPI_CUDA(cudaMemcpyAsync(h, scan + n - 1, 4, cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaMemcpyAsync(h + 1, flags + n - 1, 4, cudaMemcpyDeviceToHost, st_));
+  if (extra) EPI_CUDA(cudaMemcpyAsync(h + 2, extra, 8, cudaMemcpyDeviceToHost, st_));
   EPI_CUDA(cudaStreamSynchronize(st_));
-  return last_scan + last_flag;
+  if (extra_out) std::memcpy(extra_out, h + 2, 8);
+  return h[0] + h[1];
 }
 
 // Counts of the device-resident candidate set `c` into d_counts: exact, or
@@ -250,8 +254,12 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   stats.episodes += n;
   uint32_t bits = 1;
   while ((1ull << bits) < stream_.alphabet + 1ull) ++bits;
+  // Pass 1 only pays when a level is large and its type sequences repeat:
+  // small levels (< kMinPass1 candidates) are cheaper to count exactly than
+  // to sort, group, count hulls and gather survivors.
+  constexpr uint64_t kMinPass1 = 16384;
   const bool grouping = mode == EPI_MODE_MINE && threshold > 1 && L >= 2 && bits * L <= 64 &&
-                        n < (1ull << 31);
+                        n >= kMinPass1 && n < (1ull << 31);
   if (!grouping) {
     stats.pass2_episodes += n;
     count_device(c, d_counts, stats, &stats.pass2_ms);
@@ -280,6 +288,13 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   EPI_CUDA(cudaGetLastError());
   const uint32_t n_groups = dev_exclusive_scan(flags, scan, n);
   stats.kernel_launches += 4;
+  if (2ull * n_groups > n) {
+    // type sequences barely repeat: relaxed counts would cost as much as
+    // the exact ones, so count everything exactly
+    stats.pass2_episodes += n;
+    count_device(c, d_counts, stats, &stats.pass2_ms);
+    return;
+  }
 
   // group metadata + relaxed (hull) episodes
   const size_t g_types = 0, g_win = align256(static_cast<size_t>(n_groups) * L * 4),
@@ -319,9 +334,8 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
                                                uniform_win == 0, d_counts, sflags, d_pruned);
   EPI_CUDA(cudaGetLastError());
   uint32_t* sscan = scan;
-  const uint32_t m = dev_exclusive_scan(sflags, sscan, n);
   unsigned long long pruned = 0;
-  EPI_CUDA(cudaMemcpy(&pruned, d_pruned, 8, cudaMemcpyDeviceToHost));
+  const uint32_t m = dev_exclusive_scan(sflags, sscan, n, d_pruned, &pruned);
   stats.pruned += pruned;
   stats.kernel_launches += 2;
   stats.pass2_episodes += m;
