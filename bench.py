@@ -184,11 +184,15 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     from paper_0905_2203_b200 import Context, MODE_MINE, generate_arrays, _native
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = local_rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    # collectives on device tensors for NCCL; gloo (EPI_BENCH_BACKEND, for
+    # functional runs with several ranks on one GPU) takes host tensors
+    coll_dev = dev if os.environ.get("EPI_BENCH_BACKEND", "nccl") == "nccl" else None
     types, times = generate_arrays(make_config(args.config))
     n = len(types)
-    ctx = Context(local_rank)
+    ctx = Context(gpu)
     ctx.load_arrays(types, times, 26 if args.config != "cfg3" else 64)
     alphabet = 26 if args.config != "cfg3" else 64
 
@@ -197,20 +201,46 @@ def run_ours(args, rank, world, local_rank):
     h_times = torch.from_numpy(times).pin_memory()
     ht, htm = h_types.numpy(), h_times.numpy()
 
+    # Multi-GPU: each rank counts its episode shard; one all_gather of the
+    # u64 counts per level over NCCL (paper_0905_2203_b200/shard.py).
+    from paper_0905_2203_b200.shard import count_sharded, mine_sharded
+    acc = []
+
+    def count_fn(part, threshold, mode):
+        c = ctx.count_csr(part, threshold, mode)
+        acc.append((len(part), ctx.last_stats))
+        return c
+
+    def merged():
+        keys = acc[0][1].keys() if acc else []
+        st = {k: sum(s[k] for _, s in acc) for k in keys}
+        if acc:
+            st["segments"] = acc[-1][1]["segments"]
+        return sum(u for u, _ in acc), st
+
     if args.config == "cfg2":
-        def step():
-            cands, offs, ms, csr, counts, st = ctx.mine_raw(250, BINS, 4, MODE_MINE)
-            return sum(cands), st
+        if world == 1:
+            def step():
+                cands, offs, ms, csr, counts, st = ctx.mine_raw(250, BINS, 4, MODE_MINE)
+                return sum(cands), st
+        else:
+            def step():
+                acc.clear()
+                mine_sharded(26, 250, BINS, 4, count_fn, device=coll_dev, mode=MODE_MINE)
+                return merged()
         workload = {"workload": "cfg2: Sym26 mining to level 4, 3 bins, threshold 250, two-pass",
                     "events": n, "levels": 4, "threshold": 250, "bins": BINS}
     else:
         eps = cfg1_candidates() if args.config == "cfg1" else cfg3_candidates()
-        shard = eps[rank * len(eps) // world:(rank + 1) * len(eps) // world]
-        csr = to_csr(shard)
+        csr_all = to_csr(eps)
 
         def step():
-            ctx.count_csr(csr)
-            return len(csr), ctx.last_stats
+            acc.clear()
+            if world == 1:
+                count_fn(csr_all, 1, 0)
+            else:
+                count_sharded(csr_all, count_fn, device=coll_dev)
+            return merged()
         workload = {"workload": f"{args.config}: exact counts of {len(eps)} candidates",
                     "events": n, "candidates": len(eps)}
 
@@ -240,15 +270,16 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     barrier()
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         t_ms, cand_total, stats = timed(step, args.steps)
     clocks = clk.summary()
     step_ms = float(np.sum(t_ms))
+    red_dev = coll_dev if coll_dev is not None else torch.device("cpu")
     if world > 1:
-        tt = torch.tensor([step_ms], device=dev)
+        tt = torch.tensor([step_ms], device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms = float(tt.item())
-        ct = torch.tensor([cand_total], device=dev, dtype=torch.float64)
+        ct = torch.tensor([cand_total], device=red_dev, dtype=torch.float64)
         dist.all_reduce(ct)
         cand_total = float(ct.item())
     value = cand_total * n / (step_ms * 1e-3)
@@ -262,10 +293,10 @@ def run_ours(args, rank, world, local_rank):
     e_ms, e_units, e_stats = timed(e2e_step, args.steps)
     e_total_ms = float(np.sum(e_ms))
     if world > 1:
-        tt = torch.tensor([e_total_ms], device=dev)
+        tt = torch.tensor([e_total_ms], device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_total_ms = float(tt.item())
-        ct = torch.tensor([e_units], device=dev, dtype=torch.float64)
+        ct = torch.tensor([e_units], device=red_dev, dtype=torch.float64)
         dist.all_reduce(ct)
         e_units = float(ct.item())
     e2e_value = e_units * n / (e_total_ms * 1e-3)
@@ -280,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
     matched = sum(s["matched_pairs"] for s in stats)
     tiles = sum(s["tile_steps"] for s in stats)
     total_dev_ms = sum(s["total_ms"] for s in stats)
-    peak = ctypes_probe(_native, local_rank)
+    peak = ctypes_probe(_native, gpu)
     achieved = matched / (map_ms * 1e-3) / 1e12 if map_ms > 0 else 0.0
     roofline = {"bound": "int32", "model": "matched pairs (SURVEY 8d): 1 int op per "
                 "(episode, event of an episode type)", "achieved": round(achieved, 4),
@@ -400,8 +431,13 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("EPI_BENCH_BACKEND", "nccl")
+        gpu = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(gpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(out), flush=True)
