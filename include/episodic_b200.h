@@ -151,6 +151,18 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
                         uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
 void epi_free(void* p);
 
+/* MEA-culture-shaped bursty generator (no reference
+ * counterpart): per-electrode lognormal base rates (base_rate_hz *
+ * exp(rate_sigma * N(0,1))), network bursts as a Poisson process at
+ * burst_rate_hz lasting uniform [burst_min_ms, burst_max_ms] during which
+ * every electrode fires burst_gain times faster, plus embedded episodes as in
+ * epi_generate. Deterministic under `seed`; same output conventions. */
+epi_status epi_generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz,
+                               double rate_sigma, double burst_rate_hz, double burst_min_ms,
+                               double burst_max_ms, double burst_gain, uint64_t seed,
+                               const epi_episode_batch* embedded, const double* rates,
+                               uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
+
 /* generate_candidates (miner.hpp:76-109) exposed for parity tests and for
  * callers that drive their own level loop: `frequent` holds level-1 frequent
  * episodes (all of length level-1; ignored for level 1). Host-only (no device

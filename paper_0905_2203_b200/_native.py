@@ -58,7 +58,8 @@ class MineResult(C.Structure):
 # Symbols every build must export (checked by the CPU test-suite).
 EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "epi_load_stream",
            "epi_load_stream_device", "epi_stream_size", "epi_count", "epi_mine", "epi_generate",
-           "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32")
+           "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
+           "epi_generate_bursty")
 
 
 def _load() -> C.CDLL:
@@ -82,6 +83,10 @@ def _load() -> C.CDLL:
                                    C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p), C.POINTER(i64p),
                                    u64p]),
         "epi_free": (None, [C.c_void_p]),
+        "epi_generate_bursty": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                          C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p),
+                                          C.POINTER(i64p), u64p]),
         "epi_generate_candidates": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(EpisodeBatch), i64p, i64p,
                                               C.c_uint64, C.c_uint32, C.POINTER(EpisodeBatch)]),
         "epi_version": (C.c_char_p, []),

@@ -414,6 +414,10 @@ def generate_arrays(cfg: GenConfig):
                             C.byref(csr.struct) if csr is not None else None,
                             N.ptr(rates, C.c_double) if len(rates) else None,
                             C.byref(tp), C.byref(tm), C.byref(n))
+    return _take_stream(st, tp, tm, n)
+
+
+def _take_stream(st, tp, tm, n):
     if st != N.EPI_OK:
         _raise(st, N.lib.epi_last_error(None).decode())
     try:
@@ -424,6 +428,38 @@ def generate_arrays(cfg: GenConfig):
         N.lib.epi_free(C.cast(tp, C.c_void_p))
         N.lib.epi_free(C.cast(tm, C.c_void_p))
     return types, times
+
+
+@dataclass
+class BurstConfig:
+    """MEA-shaped bursty stream (no reference
+    counterpart): lognormal per-electrode rates, network bursts, embedded
+    episodes."""
+    electrodes: int = 60
+    duration_s: float = 100.0
+    base_rate_hz: float = 5.0
+    rate_sigma: float = 0.5
+    burst_rate_hz: float = 0.2
+    burst_min_ms: float = 100.0
+    burst_max_ms: float = 300.0
+    burst_gain: float = 20.0
+    embedded: list = field(default_factory=list)
+    seed: int = 0
+
+
+def generate_bursty_arrays(cfg: BurstConfig):
+    eps = [e.episode for e in cfg.embedded]
+    csr = episodes_to_csr(eps) if eps else None
+    rates = np.array([e.rate_hz for e in cfg.embedded], dtype=np.float64)
+    tp, tm, n = N.u32p(), N.i64p(), C.c_uint64()
+    st = N.lib.epi_generate_bursty(int(cfg.electrodes), float(cfg.duration_s), float(cfg.base_rate_hz),
+                                   float(cfg.rate_sigma), float(cfg.burst_rate_hz),
+                                   float(cfg.burst_min_ms), float(cfg.burst_max_ms),
+                                   float(cfg.burst_gain), int(cfg.seed) & ((1 << 64) - 1),
+                                   C.byref(csr.struct) if csr is not None else None,
+                                   N.ptr(rates, C.c_double) if len(rates) else None,
+                                   C.byref(tp), C.byref(tm), C.byref(n))
+    return _take_stream(st, tp, tm, n)
 
 
 def generate(cfg: GenConfig) -> EventStream:

@@ -24,11 +24,33 @@ namespace epi {
 void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
                      const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
                      std::vector<int64_t>& times);
+void generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                     double burst_rate_hz, double burst_min_ms, double burst_max_ms,
+                     double burst_gain, uint64_t seed, const epi_episode_batch* emb,
+                     const double* rates, std::vector<uint32_t>& types, std::vector<int64_t>& times);
 }
 
 namespace {
 
 thread_local std::string g_free_err;
+
+// malloc'd copies released by epi_free.
+void export_stream(const std::vector<uint32_t>& t, const std::vector<int64_t>& tm,
+                   uint32_t** types_out, int64_t** times_out, uint64_t* n_out) {
+  const size_t n = t.size();
+  auto* a = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (n ? n : 1)));
+  auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n ? n : 1)));
+  if (!a || !b) {
+    std::free(a);
+    std::free(b);
+    throw std::bad_alloc();
+  }
+  std::memcpy(a, t.data(), n * sizeof(uint32_t));
+  std::memcpy(b, tm.data(), n * sizeof(int64_t));
+  *types_out = a;
+  *times_out = b;
+  *n_out = n;
+}
 
 template <class F>
 epi_status guarded(std::string& err, F&& f) {
@@ -124,23 +146,26 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
     std::vector<uint32_t> t;
     std::vector<int64_t> tm;
     epi::generate_stream(neurons, duration_s, base_rate_hz, seed, embedded, rates, t, tm);
-    const size_t n = t.size();
-    auto* a = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (n ? n : 1)));
-    auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n ? n : 1)));
-    if (!a || !b) {
-      std::free(a);
-      std::free(b);
-      throw std::bad_alloc();
-    }
-    std::memcpy(a, t.data(), n * sizeof(uint32_t));
-    std::memcpy(b, tm.data(), n * sizeof(int64_t));
-    *types_out = a;
-    *times_out = b;
-    *n_out = n;
+    export_stream(t, tm, types_out, times_out, n_out);
   });
 }
 
 void epi_free(void* p) { std::free(p); }
+
+epi_status epi_generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz,
+                               double rate_sigma, double burst_rate_hz, double burst_min_ms,
+                               double burst_max_ms, double burst_gain, uint64_t seed,
+                               const epi_episode_batch* embedded, const double* rates,
+                               uint32_t** types_out, int64_t** times_out, uint64_t* n_out) {
+  if (!types_out || !times_out || !n_out) return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    std::vector<uint32_t> t;
+    std::vector<int64_t> tm;
+    epi::generate_bursty(electrodes, duration_s, base_rate_hz, rate_sigma, burst_rate_hz,
+                         burst_min_ms, burst_max_ms, burst_gain, seed, embedded, rates, t, tm);
+    export_stream(t, tm, types_out, times_out, n_out);
+  });
+}
 
 epi_status epi_generate_candidates(epi_ctx* ctx, uint64_t level, const epi_episode_batch* frequent,
                                    const int64_t* alpha_low, const int64_t* alpha_high,

@@ -94,16 +94,8 @@ void parallel_sort(std::vector<Ev>& v) {
   if (src != &v) v.swap(*src);
 }
 
-}  // namespace
-
-// Returns the generated stream; throws Error(EPI_EINVAL) with the
-// reference's messages (E/datagen.hpp:72-80).
-void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
-                     const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
-                     std::vector<int64_t>& times) {
-  if (neurons < 1) throw Error(EPI_EINVAL, "generate: need at least one neuron");
-  if (duration_s < 0) throw Error(EPI_EINVAL, "generate: negative duration");
-  if (!(base_rate_hz > 0)) throw Error(EPI_EINVAL, "generate: base rate must be > 0");
+// validate(Episode) + rate + neuron checks of generate() (E/datagen.hpp:75-80).
+void validate_embedded(uint32_t neurons, const epi_episode_batch* emb, const double* rates) {
   const uint64_t ne = emb ? emb->n_episodes : 0;
   for (uint64_t e = 0; e < ne; ++e) {
     uint32_t b0 = emb->offsets[e], N = emb->offsets[e + 1] - b0;
@@ -117,6 +109,20 @@ void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, u
       if (emb->types[b0 + k] >= neurons)
         throw Error(EPI_EINVAL, "generate: embedded episode references unknown neuron");
   }
+}
+
+}  // namespace
+
+// Returns the generated stream; throws Error(EPI_EINVAL) with the
+// reference's messages (E/datagen.hpp:72-80).
+void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                     const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
+                     std::vector<int64_t>& times) {
+  if (neurons < 1) throw Error(EPI_EINVAL, "generate: need at least one neuron");
+  if (duration_s < 0) throw Error(EPI_EINVAL, "generate: negative duration");
+  if (!(base_rate_hz > 0)) throw Error(EPI_EINVAL, "generate: base rate must be > 0");
+  validate_embedded(neurons, emb, rates);
+  const uint64_t ne = emb ? emb->n_episodes : 0;
 
   std::vector<std::vector<Ev>> per(neurons + ne);
   parallel_for(neurons + ne, [&](size_t j) {
@@ -159,6 +165,99 @@ void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, u
   types.resize(total);
   times.resize(total);
   for (size_t i = 0; i < total; ++i) {
+    types[i] = all[i].type;
+    times[i] = all[i].time;
+  }
+}
+
+// MEA-culture-shaped bursty generator (the reference
+// generator has no burst model, E/datagen.hpp:91-98). Deterministic under a
+// seed, with the reference's Rng (mt19937_64 raw output + splitmix64 seeds):
+//   * electrode e fires as a homogeneous Poisson process at
+//     r_e = base_rate * exp(rate_sigma * z_e), z_e ~ N(0,1) (Box-Muller),
+//     Rng(splitmix64(seed ^ (0xB0B5 + e)));
+//   * network bursts start as a Poisson process at burst_rate_hz and last
+//     uniform [burst_min_ms, burst_max_ms], Rng(splitmix64(seed ^ 0xB1257));
+//     inside a burst every electrode fires additionally at
+//     r_e * (burst_gain - 1) (so the total rate is burst_gain * r_e);
+//   * embedded episodes exactly as generate(): exponential starts, uniform
+//     gaps inside each constraint window;
+//   * events sorted by (time, type); times truncated to ms.
+void generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                     double burst_rate_hz, double burst_min_ms, double burst_max_ms,
+                     double burst_gain, uint64_t seed, const epi_episode_batch* emb,
+                     const double* rates, std::vector<uint32_t>& types,
+                     std::vector<int64_t>& times) {
+  if (electrodes < 1) throw Error(EPI_EINVAL, "generate: need at least one neuron");
+  if (duration_s < 0) throw Error(EPI_EINVAL, "generate: negative duration");
+  if (!(base_rate_hz > 0)) throw Error(EPI_EINVAL, "generate: base rate must be > 0");
+  if (!(burst_gain >= 1) || burst_rate_hz < 0 || burst_min_ms < 0 || burst_max_ms < burst_min_ms)
+    throw Error(EPI_EINVAL, "generate_bursty: invalid burst parameters");
+  // burst schedule (shared by every electrode)
+  std::vector<std::pair<double, double>> bursts;  // [start, end) in seconds
+  if (burst_rate_hz > 0) {
+    Rng rb(splitmix64(seed ^ 0xB1257ULL));
+    double t = rb.exponential(burst_rate_hz);
+    while (t < duration_s) {
+      const double len = (burst_min_ms + (burst_max_ms - burst_min_ms) * rb.uniform01()) / 1000.0;
+      bursts.emplace_back(t, std::min(t + len, duration_s));
+      t += len + rb.exponential(burst_rate_hz);
+    }
+  }
+  validate_embedded(electrodes, emb, rates);
+  // background + bursts per electrode
+  std::vector<std::vector<Ev>> per(electrodes);
+  parallel_for(electrodes, [&](size_t j) {
+    const uint32_t e = static_cast<uint32_t>(j);
+    Rng rng(splitmix64(seed ^ (0xB0B5ULL + e)));
+    const double u1 = rng.uniform01(), u2 = rng.uniform01();
+    const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+    const double r = base_rate_hz * std::exp(rate_sigma * z);
+    std::vector<Ev>& out = per[j];
+    double t = rng.exponential(r);
+    while (t < duration_s) {
+      out.push_back({static_cast<int64_t>(t * 1000.0), e});
+      t += rng.exponential(r);
+    }
+    const double extra = r * (burst_gain - 1.0);
+    if (extra > 0)
+      for (const auto& b : bursts) {
+        double s = b.first + rng.exponential(extra);
+        while (s < b.second) {
+          out.push_back({static_cast<int64_t>(s * 1000.0), e});
+          s += rng.exponential(extra);
+        }
+      }
+  });
+  size_t total = 0;
+  for (auto& v : per) total += v.size();
+  std::vector<Ev> all;
+  all.reserve(total);
+  for (auto& v : per) {
+    all.insert(all.end(), v.begin(), v.end());
+    std::vector<Ev>().swap(v);
+  }
+  // embedded episodes: same RNG streams as generate()
+  const uint64_t ne = emb ? emb->n_episodes : 0;
+  for (uint64_t e = 0; e < ne; ++e) {
+    const uint32_t b0 = emb->offsets[e], N = emb->offsets[e + 1] - b0;
+    const uint64_t cb = b0 - e;
+    Rng rng(splitmix64(seed ^ (0xE1BEDDEDULL + (e << 20))));
+    double start_s = rng.exponential(rates[e]);
+    while (start_s < duration_s) {
+      int64_t t = static_cast<int64_t>(start_s * 1000.0);
+      all.push_back({t, emb->types[b0]});
+      for (uint32_t k = 1; k < N; ++k) {
+        t += rng.uniform_gap(emb->low[cb + k - 1], emb->high[cb + k - 1]);
+        all.push_back({t, emb->types[b0 + k]});
+      }
+      start_s += rng.exponential(rates[e]);
+    }
+  }
+  parallel_sort(all);
+  types.resize(all.size());
+  times.resize(all.size());
+  for (size_t i = 0; i < all.size(); ++i) {
     types[i] = all[i].type;
     times[i] = all[i].time;
   }
