@@ -97,7 +97,10 @@ __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t
   uint32_t zl, zh;
   if constexpr (kHi32 && W > 0) {
     // X = (c : h1); term b of the smear is (c : h1) >> (32 - hi + b), and
-    // 32 - hi + b <= 32 - lo1 <= 31, so each term is one funnel shift.
+    // 32 - hi + b <= 32 - lo1 <= 31, so each term is one funnel shift (ALU
+    // pipe). (Moving terms to the FMA pipe as hi32(h1*m + ((c*m) << 32))
+    // with m = 2^(hi-b) was measured 33% slower: nvcc kept the shifts and
+    // split the 64-bit add onto the ALU pipe.)
     const uint32_t s = 32u - hi;
     uint32_t d = __funnelshift_r(h1, c, s);
 #pragma unroll
