@@ -285,3 +285,41 @@ def test_cfg3_first_candidates(ctx, golden_configs):
     got = ctx.count_csr(csr_of(eps))
     assert [int(x) for x in got] == g["counts"]
     assert int(got[:64].sum()) == g["sum_first64"] == 87180
+
+
+@pytest.mark.parametrize("alphabet", [300, 1000, 4000])
+def test_large_alphabets(ctx, alphabet):
+    """Bitmap blocks beyond the shared-memory ring (alphabet > ~340 types read
+    rows from global memory) and the spare zero row."""
+    rng = np.random.default_rng(alphabet)
+    n = 60000
+    times = np.cumsum(rng.integers(0, 3, n)).astype(np.int64)
+    hot = rng.integers(0, 20, n)          # a few frequent types so counts are non-zero
+    types = np.where(rng.random(n) < 0.7, hot, rng.integers(0, alphabet, n)).astype(np.uint32)
+    eps = [([int(a), int(b), int(c)], [(0, 5), (2, 9)]) for a, b, c in rng.integers(0, 20, (150, 3))]
+    eps += [([int(a), int(b)], [(1, 30)]) for a, b in rng.integers(0, alphabet, (100, 2))]
+    got = count_one(ctx, types, times, alphabet, eps)
+    csr = csr_of(eps)
+    want = oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=8)
+    np.testing.assert_array_equal(got, want)
+    assert int(got.sum()) > 0
+
+
+def test_million_candidates(ctx):
+    """10^6 candidates in one batch (cfg5's largest candidate set) on a 1M
+    event stream: seeded subset against the oracle."""
+    rng = np.random.default_rng(7)
+    types, times = generate_arrays(GenConfig(64, 1_000_000 / (64 * 20), 20, [], 77))
+    ctx.load_arrays(types, times, 64)
+    m = 1_000_000
+    t = rng.integers(0, 64, (m, 3)).astype(np.uint32)
+    b = rng.integers(0, 3, (m, 2))
+    lo = np.array([0, 5, 10], np.int64)[b].reshape(-1)
+    from paper_0905_2203_b200 import CSR
+    csr = CSR(np.arange(0, 3 * m + 1, 3, dtype=np.uint32), t.reshape(-1), lo, lo + 5)
+    got = ctx.count_csr(csr)
+    pick = np.sort(rng.choice(m, 64, replace=False))
+    sub = csr_of([([int(x) for x in t[i]], [(int(lo[2 * i]), int(lo[2 * i]) + 5),
+                                            (int(lo[2 * i + 1]), int(lo[2 * i + 1]) + 5)]) for i in pick])
+    want = oracle.count_batch(types, times, sub.offsets, sub.types, sub.low, sub.high, threads=16)
+    np.testing.assert_array_equal(got[pick], want)
