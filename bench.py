@@ -313,10 +313,22 @@ def run_ours(args, rank, world, local_rank):
     total_dev_ms = sum(s["total_ms"] for s in stats)
     peak = ctypes_probe(_native, gpu)
     achieved = matched / (map_ms * 1e-3) / 1e12 if map_ms > 0 else 0.0
+    # DRAM bytes per launch of the same kernel from the committed ncu --set
+    # full capture (profiles/roofline_traffic.json, scripts/traffic_json.py)
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            tj = json.load(f).get(args.config)
+        if tj:
+            traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "int32", "model": "matched pairs (SURVEY 8d): 1 int op per "
                 "(episode, event of an episode type)", "achieved": round(achieved, 4),
                 "peak": round(peak, 3), "unit": "Tops/s", "frac": round(achieved / peak, 5) if peak else None,
-                "traffic": None, "peak_source": "epi_probe_int32 (LOP3+IMAD, measured in this run)",
+                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu)",
+                "traffic_source": traffic_src,
+                "peak_source": "epi_probe_int32 (LOP3+IMAD, measured in this run)",
                 "kernel": "machines_kernel", "launches": map_launches,
                 "avg_launch_ms": round(map_ms / max(map_launches, 1), 5),
                 "share_of_device_time": round(map_ms / total_dev_ms, 4) if total_dev_ms else None,

@@ -12,3 +12,6 @@ if [ "${NCU:-1}" = 1 ]; then
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cfg2.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:machines_kernel -s 2 -c 1 -o gpurun_out/prof_cfg3 -f python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_cfg3.log 2>&1
 fi
+if [ "${NCU:-1}" = 1 ]; then
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:NarrowHist<.int.3, .int.5" -s 1 -c 1 -o gpurun_out/prof_cfg2 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_cfg2.log 2>&1
+fi

@@ -1,0 +1,29 @@
+"""Per-launch DRAM traffic of the bench configs' dominant kernels from the
+committed ncu captures -> profiles/roofline_traffic.json (read by bench.py)."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+out = {}
+for cfg, rep, summary in [("cfg2", "gpurun_out/prof_cfg2.ncu-rep", "profiles/r01_cfg2_machines_kernel_ncu.txt"),
+                          ("cfg3", "gpurun_out/prof_cfg3.ncu-rep", "profiles/r01_cfg3_machines_kernel_ncu.txt")]:
+    try:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        col = {h: (u, v) for h, u, v in zip(hdr, units, vals)}
+
+        def nbytes(name):
+            u, v = col[name]
+            return float(v.replace(",", "")) * SCALE[u]
+        out[cfg] = {"kernel": col.get("Kernel Name", ("", ""))[1],
+                    "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
+                    "source": summary}
+    except Exception as e:  # capture missing
+        print(cfg, "skipped:", e, file=sys.stderr)
+json.dump(out, open("profiles/roofline_traffic.json", "w"), indent=1)
+print(json.dumps(out, indent=1))
