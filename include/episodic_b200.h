@@ -108,6 +108,20 @@ epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t thre
                      uint32_t mode, uint64_t* counts_out, uint8_t* frequent_out,
                      epi_stats* stats);
 
+/* Parallel local tracking (the paper's Alg. 2; tracking.hpp:236-407) on the
+ * device, a second exact counter with the reference's interval output.
+ * direction: 0 forward (tracking from the first type), 1 backward.
+ *   epi_find_occurrences  find_occurrences (tracking.hpp:330-367): the
+ *                         intervals of episode e are starts/ends[off[e] ..
+ *                         off[e+1]) in the reference's order; the three
+ *                         arrays are library-allocated (release with epi_free).
+ *   epi_count_tracking    count_tracking (tracking.hpp:391-407): tracking +
+ *                         greedy_schedule, equal to count_fsm on every input. */
+epi_status epi_find_occurrences(epi_ctx* ctx, const epi_episode_batch* batch, uint32_t direction,
+                                uint64_t** offsets_out, int64_t** starts_out, int64_t** ends_out);
+epi_status epi_count_tracking(epi_ctx* ctx, const epi_episode_batch* batch, uint32_t direction,
+                              uint64_t* counts_out, epi_stats* stats);
+
 /* Level-wise mining, mine() (miner.hpp:114-173) with one epi_count call per
  * level. The result is owned by the context until the next epi_mine call:
  *   *n_levels                     levels produced

@@ -89,6 +89,9 @@ def ref():
                                      i64p, C.POINTER(C.c_double), C.c_uint64, C.POINTER(u32p),
                                      C.POINTER(i64p), u64p]
         lib.ref_free.argtypes = [C.c_void_p]
+        lib.ref_find_occurrences.restype = C.c_int
+        lib.ref_find_occurrences.argtypes = [u32p, i64p, C.c_uint64, C.c_uint32, u32p, u32p, i64p, i64p,
+                                             C.c_int, C.POINTER(i64p), C.POINTER(i64p), u64p]
         lib.ref_default_workers.restype = C.c_uint
         _ref = lib
     return _ref
@@ -183,6 +186,25 @@ def ref_mine(types, times, alphabet, threshold, bins, max_level, switch_level=3,
     lib.ref_free(C.cast(csv, C.c_void_p))
     k = int(nl.value)
     return text, [int(x) for x in cands[:k]], [float(ms[i]) for i in range(k)]
+
+
+def ref_find_occurrences(types, times, alphabet, ep_types, low, high, direction=0):
+    """find_occurrences of the reference for one episode -> [(start, end)]."""
+    lib = ref()
+    t, tm = _u32(types), _i64(times)
+    et, lo, hi = _u32(ep_types), _i64(low), _i64(high)
+    off = _u32([0, len(et)])
+    sp, ep, n = i64p(), i64p(), C.c_uint64()
+    st = lib.ref_find_occurrences(_p(t, C.c_uint32), _p(tm, C.c_int64), len(t), alphabet,
+                                  _p(off, C.c_uint32), _p(et, C.c_uint32), _p(lo, C.c_int64),
+                                  _p(hi, C.c_int64), direction, C.byref(sp), C.byref(ep), C.byref(n))
+    if st != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    k = int(n.value)
+    out = [(sp[i], ep[i]) for i in range(k)]
+    lib.ref_free(C.cast(sp, C.c_void_p))
+    lib.ref_free(C.cast(ep, C.c_void_p))
+    return out
 
 
 def ref_default_workers() -> int:

@@ -181,6 +181,34 @@ int ref_generate(uint32_t neurons, double duration_s, double base_rate_hz, uint6
   }
 }
 
+// find_occurrences (E/tracking.hpp:330-367) for one episode (CSR with one
+// entry); direction 0 forward, 1 backward. Outputs malloc'd (ref_free).
+int ref_find_occurrences(const uint32_t* types, const int64_t* times, uint64_t n, uint32_t alphabet,
+                         const uint32_t* off, const uint32_t* ep_types, const int64_t* lo,
+                         const int64_t* hi, int direction, int64_t** starts_out,
+                         int64_t** ends_out, uint64_t* n_out) {
+  try {
+    EventStream s = make_stream(types, times, n, alphabet);
+    std::vector<Episode> eps = make_episodes(off, ep_types, lo, hi, 1);
+    TypeIndex index = build_index(s);
+    TrackingOptions opt;
+    opt.direction = direction ? Direction::backward : Direction::forward;
+    std::vector<OccurrenceInterval> occ = find_occurrences(s, index, eps[0], opt);
+    auto* a = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (occ.size() + 1)));
+    auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (occ.size() + 1)));
+    for (size_t i = 0; i < occ.size(); ++i) {
+      a[i] = occ[i].start;
+      b[i] = occ[i].end;
+    }
+    *starts_out = a;
+    *ends_out = b;
+    *n_out = occ.size();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 void ref_free(void* p) { std::free(p); }
 
 unsigned ref_default_workers() { return default_workers(); }

@@ -250,6 +250,31 @@ class Context:
         self.load(stream)
         return self.count_csr(episodes_to_csr(episodes), threshold, mode)
 
+    def count_tracking_csr(self, csr: N.CSR, direction: int = 0):
+        """Parallel local tracking + greedy on the device (epi_count_tracking)."""
+        counts = np.zeros(len(csr), dtype=np.uint64)
+        stats = N.Stats()
+        self._check(N.lib.epi_count_tracking(self._h, C.byref(csr.struct), int(direction),
+                                             N.ptr(counts, C.c_uint64), C.byref(stats)))
+        self.last_stats = stats.as_dict()
+        return counts
+
+    def find_occurrences_csr(self, csr: N.CSR, direction: int = 0):
+        """(offsets, starts, ends) of every episode's occurrence intervals."""
+        op, sp, ep = N.u64p(), N.i64p(), N.i64p()
+        self._check(N.lib.epi_find_occurrences(self._h, C.byref(csr.struct), int(direction),
+                                               C.byref(op), C.byref(sp), C.byref(ep)))
+        try:
+            n = len(csr)
+            off = np.ctypeslib.as_array(op, shape=(n + 1,)).copy()
+            tot = int(off[-1])
+            s = np.ctypeslib.as_array(sp, shape=(max(tot, 1),))[:tot].copy()
+            e = np.ctypeslib.as_array(ep, shape=(max(tot, 1),))[:tot].copy()
+        finally:
+            for ptr_ in (op, sp, ep):
+                N.lib.epi_free(C.cast(ptr_, C.c_void_p))
+        return off, s, e
+
     def mine_raw(self, threshold: int, bins: Sequence, max_level: int, mode: int = N.MODE_MINE):
         lo = np.array([b[0] for b in bins], dtype=np.int64)
         hi = np.array([b[1] for b in bins], dtype=np.int64)
@@ -291,10 +316,41 @@ def count_fsm(stream: EventStream, ep: Episode) -> int:
     return int(default_context().count(stream, [ep])[0])
 
 
+@dataclass
+class TrackingOptions:
+    """TrackingOptions, E/tracking.hpp:33-39. direction is used; the CPU
+    compaction strategy, workers and slab width have no device meaning (the
+    device compacts with a block scan) and are accepted for parity."""
+    direction: str = "forward"
+    strategy: str = "count_scan_write"
+    workers: int = 1
+    flag_slots: int = 32
+
+
+def _direction(opt) -> int:
+    d = getattr(opt, "direction", "forward") if opt is not None else "forward"
+    return 1 if str(d).lower().endswith("backward") else 0
+
+
 def count_tracking(stream: EventStream, index, ep: Episode, opt=None, stats=None) -> int:
-    """count_tracking, E/tracking.hpp:391-407: equal to count_fsm on every
-    input; the index, options and stats are accepted for signature parity."""
-    return count_fsm(stream, ep)
+    """count_tracking, E/tracking.hpp:391-407, on the device: parallel local
+    tracking + greedy_schedule (equal to count_fsm on every input). `index`
+    is accepted for signature parity (the device builds its own)."""
+    validate(ep)
+    ctx = default_context()
+    ctx.load(stream)
+    return int(ctx.count_tracking_csr(episodes_to_csr([ep]), _direction(opt))[0])
+
+
+def find_occurrences(stream: EventStream, index, ep: Episode, opt=None, stats=None) -> list:
+    """find_occurrences, E/tracking.hpp:330-367, on the device: the
+    representative occurrence intervals [(start, end)] in the reference's
+    order."""
+    validate(ep)
+    ctx = default_context()
+    ctx.load(stream)
+    off, s, e = ctx.find_occurrences_csr(episodes_to_csr([ep]), _direction(opt))
+    return [(int(a), int(b)) for a, b in zip(s, e)]
 
 
 def count_mapconcat(stream: EventStream, ep: Episode, segments: int, workers: int = 1,

@@ -132,6 +132,41 @@ epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t thre
   });
 }
 
+epi_status epi_find_occurrences(epi_ctx* ctx, const epi_episode_batch* batch, uint32_t direction,
+                                uint64_t** offsets_out, int64_t** starts_out, int64_t** ends_out) {
+  if (!ctx || !batch || !offsets_out || !starts_out || !ends_out) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    std::vector<uint64_t> off;
+    std::vector<int64_t> s, e;
+    ctx->engine.track_batch(*batch, direction, nullptr, &off, &s, &e, nullptr);
+    auto* o = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * off.size()));
+    auto* a = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (s.size() ? s.size() : 1)));
+    auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (e.size() ? e.size() : 1)));
+    if (!o || !a || !b) {
+      std::free(o);
+      std::free(a);
+      std::free(b);
+      throw std::bad_alloc();
+    }
+    std::memcpy(o, off.data(), off.size() * sizeof(uint64_t));
+    std::memcpy(a, s.data(), s.size() * sizeof(int64_t));
+    std::memcpy(b, e.data(), e.size() * sizeof(int64_t));
+    *offsets_out = o;
+    *starts_out = a;
+    *ends_out = b;
+  });
+}
+
+epi_status epi_count_tracking(epi_ctx* ctx, const epi_episode_batch* batch, uint32_t direction,
+                              uint64_t* counts_out, epi_stats* stats) {
+  if (!ctx || !batch) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    ctx->engine.track_batch(*batch, direction, counts_out, nullptr, nullptr, nullptr, stats);
+  });
+}
+
 epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out) {
   if (!ctx || !cfg || !out) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);

@@ -125,6 +125,7 @@ void Engine::h2d(void* dst, const void* src, size_t bytes) {
 void Engine::load_stream_host(const uint32_t* types, const int64_t* times, uint64_t n,
                               uint32_t alphabet) {
   if (n && (!types || !times)) throw Error(EPI_EINVAL, "epi_load_stream: null event arrays");
+  csr_valid_ = false;
   stream_.reserve_raw(n);
   h2d(stream_.d_types_raw, types, n * sizeof(uint32_t));
   h2d(stream_.d_times_raw, times, n * sizeof(int64_t));
@@ -134,6 +135,7 @@ void Engine::load_stream_host(const uint32_t* types, const int64_t* times, uint6
 void Engine::load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,
                                 uint32_t alphabet) {
   if (n && (!d_types || !d_times)) throw Error(EPI_EINVAL, "epi_load_stream_device: null arrays");
+  csr_valid_ = false;
   stream_.reserve_raw(n);
   EPI_CUDA(cudaMemcpyAsync(stream_.d_types_raw, d_types, n * sizeof(uint32_t),
                            cudaMemcpyDeviceToDevice, st_));

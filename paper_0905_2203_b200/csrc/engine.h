@@ -77,6 +77,10 @@ class Engine {
   void count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
                    uint64_t* counts_out, uint8_t* frequent_out, epi_stats* stats);
   void mine(const epi_mine_config& cfg, epi_mine_result* out);
+  // Parallel local tracking (tracking.cu): counts (greedy) and/or intervals.
+  void track_batch(const epi_episode_batch& b, uint32_t direction, uint64_t* counts_out,
+                   std::vector<uint64_t>* off_out, std::vector<int64_t>* starts,
+                   std::vector<int64_t>* ends, epi_stats* stats_out);
 
   std::string err;
   std::mutex mu;
@@ -93,6 +97,14 @@ class Engine {
                               const unsigned long long* extra = nullptr,
                               unsigned long long* extra_out = nullptr);
   void h2d(void* dst, const void* src, size_t bytes);
+  void ensure_type_index();
+
+  // per-type index for tracking (built lazily per loaded stream)
+  bool csr_valid_ = false;
+  std::vector<uint64_t> csr_off_;
+  uint64_t csr_cap_ = 0;
+  uint64_t* d_csr_off_ = nullptr;
+  int64_t* d_csr_time_ = nullptr;
 
   int device_;
   int num_sms_ = 148;
