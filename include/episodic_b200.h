@@ -165,6 +165,16 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
                         uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
 void epi_free(void* p);
 
+/* Event-file ingest, load_stream (io.hpp:22-56) restated multi-threaded:
+ * `<name>,<int_ms>` per line, '#' comments and blank lines skipped, CRLF
+ * tolerated. Type ids are the names' first-seen order; *names_out receives
+ * the names joined by '\n' (id order). Errors are EPI_EDATA with the
+ * reference's messages and line numbers. Outputs are library-allocated
+ * (epi_free). Feed the arrays to epi_load_stream with *alphabet_out. */
+epi_status epi_parse_events(const char* text, uint64_t len, uint32_t** types_out,
+                            int64_t** times_out, uint64_t* n_out, char** names_out,
+                            uint32_t* alphabet_out);
+
 /* MEA-culture-shaped bursty generator (no reference
  * counterpart): per-electrode lognormal base rates (base_rate_hz *
  * exp(rate_sigma * N(0,1))), network bursts as a Poisson process at

@@ -93,6 +93,9 @@ def ref():
         lib.ref_find_occurrences.argtypes = [u32p, i64p, C.c_uint64, C.c_uint32, u32p, u32p, i64p, i64p,
                                              C.c_int, C.POINTER(i64p), C.POINTER(i64p), u64p]
         lib.ref_default_workers.restype = C.c_uint
+        lib.ref_load_stream.restype = C.c_int
+        lib.ref_load_stream.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(u32p), C.POINTER(i64p), u64p,
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_uint32), u64p]
         _ref = lib
     return _ref
 
@@ -205,6 +208,32 @@ def ref_find_occurrences(types, times, alphabet, ep_types, low, high, direction=
     lib.ref_free(C.cast(sp, C.c_void_p))
     lib.ref_free(C.cast(ep, C.c_void_p))
     return out
+
+
+def ref_load_stream(data: bytes):
+    """load_stream of the reference (E/io.hpp:22-56) on `data` ->
+    (types, times, names) or raises RefDataError(msg, line)."""
+    lib = ref()
+    tp, tm, n, nm = u32p(), i64p(), C.c_uint64(), C.c_void_p()
+    alpha, line = C.c_uint32(), C.c_uint64()
+    st = lib.ref_load_stream(data, len(data), C.byref(tp), C.byref(tm), C.byref(n), C.byref(nm),
+                             C.byref(alpha), C.byref(line))
+    if st != 0:
+        raise RefDataError(lib.ref_last_error().decode(), int(line.value))
+    k = int(n.value)
+    types = np.array([tp[i] for i in range(k)], dtype=np.uint32)
+    times = np.array([tm[i] for i in range(k)], dtype=np.int64)
+    names = C.string_at(nm.value).decode()
+    for q in (tp, tm):
+        lib.ref_free(C.cast(q, C.c_void_p))
+    lib.ref_free(nm)
+    return types, times, (names.split("\n") if alpha.value else [])
+
+
+class RefDataError(RuntimeError):
+    def __init__(self, msg, line):
+        super().__init__(msg)
+        self.line = line
 
 
 def ref_default_workers() -> int:

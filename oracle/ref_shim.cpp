@@ -209,6 +209,42 @@ int ref_find_occurrences(const uint32_t* types, const int64_t* times, uint64_t n
   }
 }
 
+// load_stream (E/io.hpp:22-56) on an in-memory text. Names are returned
+// '\n'-joined in id order; on DataError *line_out receives e.line.
+int ref_load_stream(const char* text, uint64_t len, uint32_t** types_out, int64_t** times_out,
+                    uint64_t* n_out, char** names_out, uint32_t* alphabet_out, uint64_t* line_out) {
+  *line_out = 0;
+  try {
+    std::istringstream in(std::string(text, len));
+    LoadedStream ls = load_stream(in);
+    const size_t n = ls.stream.size();
+    auto* a = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * (n + 1)));
+    auto* b = static_cast<int64_t*>(std::malloc(sizeof(int64_t) * (n + 1)));
+    for (size_t i = 0; i < n; ++i) {
+      a[i] = ls.stream.type_at(i);
+      b[i] = ls.stream.time_at(i);
+    }
+    std::string joined;
+    for (size_t i = 0; i < ls.symbols.size(); ++i) {
+      if (i) joined += '\n';
+      joined += ls.symbols.name(static_cast<TypeId>(i));
+    }
+    char* nm = static_cast<char*>(std::malloc(joined.size() + 1));
+    std::memcpy(nm, joined.c_str(), joined.size() + 1);
+    *types_out = a;
+    *times_out = b;
+    *n_out = n;
+    *names_out = nm;
+    *alphabet_out = static_cast<uint32_t>(ls.symbols.size());
+    return 0;
+  } catch (const DataError& e) {
+    *line_out = e.line;
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 void ref_free(void* p) { std::free(p); }
 
 unsigned ref_default_workers() { return default_workers(); }

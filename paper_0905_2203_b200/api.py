@@ -38,7 +38,12 @@ class InvalidArgument(ValueError):
 
 
 class DataError(RuntimeError):
-    """episodic::DataError (E/types.hpp:75-80)."""
+    """episodic::DataError (E/types.hpp:75-80); `line` is the 1-based input
+    line for event-file errors, 0 otherwise."""
+
+    def __init__(self, msg: str, line: int = 0):
+        super().__init__(msg)
+        self.line = line
 
 
 class Unsupported(EpisodicError):
@@ -49,7 +54,11 @@ def _raise(status: int, msg: str):
     if status == N.EPI_EINVAL:
         raise InvalidArgument(msg)
     if status == N.EPI_EDATA:
-        raise DataError(msg)
+        line = 0
+        if msg.startswith("line "):
+            head = msg[5:].split(":", 1)[0]
+            line = int(head) if head.isdigit() else 0
+        raise DataError(msg, line)
     if status == N.EPI_EOVERFLOW:
         raise OverflowError(msg)
     if status == N.EPI_EUNSUPPORTED:
@@ -521,3 +530,53 @@ def generate_bursty_arrays(cfg: BurstConfig):
 def generate(cfg: GenConfig) -> EventStream:
     types, times = generate_arrays(cfg)
     return EventStream(types, times, cfg.neurons)
+
+
+class LoadedStream(NamedTuple):
+    """LoadedStream, E/io.hpp:14-17: the stream plus its symbol names (id
+    order, first-seen)."""
+    stream: EventStream
+    symbols: list
+
+
+def load_stream(text) -> LoadedStream:
+    """load_stream, E/io.hpp:22-56, parsed natively (multi-threaded C++ in
+    csrc/io.cpp): `<name>,<int_ms>` per line; '#' comments, blank lines and
+    CRLF tolerated; DataError with the reference's message and `.line`."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    tp, tm, n = N.u32p(), N.i64p(), C.c_uint64()
+    names_p, alpha = C.c_void_p(), C.c_uint32()
+    st = N.lib.epi_parse_events(data, len(data), C.byref(tp), C.byref(tm), C.byref(n),
+                                C.byref(names_p), C.byref(alpha))
+    if st != N.EPI_OK:
+        _raise(st, N.lib.epi_last_error(None).decode())
+    try:
+        joined = C.string_at(names_p.value).decode() if names_p.value else ""
+    finally:
+        N.lib.epi_free(names_p)
+    types, times = _take_stream(st, tp, tm, n)
+    names = joined.split("\n") if alpha.value else []
+    return LoadedStream(EventStream(types, times, int(alpha.value)), names)
+
+
+def load_stream_file(path: str) -> LoadedStream:
+    """load_stream_file, E/io.hpp:58-62."""
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise DataError(f"cannot open event file '{path}'") from None
+    return load_stream(data)
+
+
+def serialize_stream(stream: EventStream, symbols=None) -> str:
+    """serialize_stream, E/io.hpp:64-67 (numeric names by default, like
+    SymbolTable::numeric)."""
+    types, times = stream.types(), stream.times()
+    if symbols is None:
+        names = types.astype(str)
+    else:
+        names = np.asarray(list(symbols), dtype=object)[types]
+    if len(types) == 0:
+        return ""
+    return "\n".join(f"{a},{b}" for a, b in zip(names.tolist(), times.tolist())) + "\n"

@@ -24,6 +24,8 @@ namespace epi {
 void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
                      const epi_episode_batch* emb, const double* rates, std::vector<uint32_t>& types,
                      std::vector<int64_t>& times);
+void parse_event_text(const char* text, size_t len, std::vector<uint32_t>& types,
+                      std::vector<int64_t>& times, std::vector<std::string>& names);
 void generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
                      double burst_rate_hz, double burst_min_ms, double burst_max_ms,
                      double burst_gain, uint64_t seed, const epi_episode_batch* emb,
@@ -186,6 +188,30 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
 }
 
 void epi_free(void* p) { std::free(p); }
+
+epi_status epi_parse_events(const char* text, uint64_t len, uint32_t** types_out,
+                            int64_t** times_out, uint64_t* n_out, char** names_out,
+                            uint32_t* alphabet_out) {
+  if (!types_out || !times_out || !n_out || !names_out || !alphabet_out || (len && !text))
+    return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    std::vector<uint32_t> t;
+    std::vector<int64_t> tm;
+    std::vector<std::string> names;
+    epi::parse_event_text(text, len, t, tm, names);
+    std::string joined;
+    for (size_t i = 0; i < names.size(); ++i) {
+      if (i) joined += '\n';
+      joined += names[i];
+    }
+    char* nm = static_cast<char*>(std::malloc(joined.size() + 1));
+    if (!nm) throw std::bad_alloc();
+    std::memcpy(nm, joined.c_str(), joined.size() + 1);
+    export_stream(t, tm, types_out, times_out, n_out);
+    *names_out = nm;
+    *alphabet_out = static_cast<uint32_t>(names.size());
+  });
+}
 
 epi_status epi_generate_bursty(uint32_t electrodes, double duration_s, double base_rate_hz,
                                double rate_sigma, double burst_rate_hz, double burst_min_ms,
