@@ -203,7 +203,7 @@ def run_ours(args, rank, world, local_rank):
 
     # Multi-GPU: each rank counts its episode shard; one all_gather of the
     # u64 counts per level over NCCL (paper_0905_2203_b200/shard.py).
-    from paper_0905_2203_b200.shard import count_sharded, mine_sharded
+    from paper_0905_2203_b200.shard import count_sharded, make_allgather
     acc = []
 
     def count_fn(part, threshold, mode):
@@ -224,10 +224,16 @@ def run_ours(args, rank, world, local_rank):
                 cands, offs, ms, csr, counts, st = ctx.mine_raw(250, BINS, 4, MODE_MINE)
                 return sum(cands), st
         else:
+            # device-resident mining on every rank; each level of >= 8192
+            # candidates is episode-sharded and its u64 counts all-gathered
+            # on the engine's stream (NCCL; gloo host-staged for functional
+            # runs of several ranks on one GPU)
+            ag = make_allgather(memory="cuda" if coll_dev is not None else "staged", device=dev)
+
             def step():
-                acc.clear()
-                mine_sharded(26, 250, BINS, 4, count_fn, device=coll_dev, mode=MODE_MINE)
-                return merged()
+                cands, offs, ms, csr, counts, st = ctx.mine_raw(250, BINS, 4, MODE_MINE,
+                                                                shard=(rank, world, 8192, ag))
+                return sum(cands) / world, st  # job units, summed over ranks below
         workload = {"workload": "cfg2: Sym26 mining to level 4, 3 bins, threshold 250, two-pass",
                     "events": n, "levels": 4, "threshold": 250, "bins": BINS}
     else:

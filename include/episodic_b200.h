@@ -152,6 +152,32 @@ typedef struct {
 
 epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out);
 
+/* Episode-sharded mining across ranks (one process and one context per GPU,
+ * SURVEY §8e). Every rank generates each level's full candidate list on its
+ * own device (the join is deterministic, so the lists agree). A level with
+ * at least min_shard candidates is cut into `world` contiguous slices of
+ * s = ceil(n / world) candidates; rank r counts slice r only, then calls
+ * allgather(user, send, recv, s * 8, stream) with send = its s u64 counts
+ * and recv = world * s u64 (both device pointers on the context's device),
+ * ordered on the context's CUDA stream `stream` (cudaStream_t). The callback
+ * must leave recv = the rank-ordered concatenation of every rank's send
+ * (an NCCL all-gather) with the work ordered before anything later enqueued
+ * on `stream`, and return 0 (nonzero -> EPI_ENCCL). Thresholding and the next
+ * join then run identically on every rank: the result equals epi_mine's on
+ * every rank. Smaller levels are counted whole on every rank. */
+typedef int (*epi_allgather_fn)(void* user, const void* send_dev, void* recv_dev,
+                                uint64_t bytes_per_rank, void* cuda_stream);
+typedef struct {
+  uint32_t rank;
+  uint32_t world;
+  uint64_t min_shard; /* levels with fewer candidates are not sharded */
+  epi_allgather_fn allgather;
+  void* user;
+} epi_shard;
+
+epi_status epi_mine_sharded(epi_ctx* ctx, const epi_mine_config* cfg, const epi_shard* shard,
+                            epi_mine_result* out);
+
 /* Synthetic spike-train generator, a bit-exact restatement of generate()
  * (datagen.hpp:71-122): per-neuron homogeneous Poisson background plus
  * injected episodes with uniform gaps, ties ordered by neuron id. The

@@ -55,11 +55,20 @@ class MineResult(C.Structure):
                 ("totals", Stats)]
 
 
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+class Shard(C.Structure):
+    _fields_ = [("rank", C.c_uint32), ("world", C.c_uint32), ("min_shard", C.c_uint64),
+                ("allgather", ALLGATHER_FN), ("user", C.c_void_p)]
+
+
 # Symbols every build must export (checked by the CPU test-suite).
 EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "epi_load_stream",
            "epi_load_stream_device", "epi_stream_size", "epi_count", "epi_mine", "epi_generate",
            "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
-           "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events")
+           "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
+           "epi_mine_sharded")
 
 
 def _load() -> C.CDLL:
@@ -79,6 +88,8 @@ def _load() -> C.CDLL:
         "epi_count": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, C.c_uint32, u64p, u8p,
                                 C.POINTER(Stats)]),
         "epi_mine": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(MineResult)]),
+        "epi_mine_sharded": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(Shard),
+                                       C.POINTER(MineResult)]),
         "epi_parse_events": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), C.POINTER(i64p), u64p,
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_uint32)]),
         "epi_find_occurrences": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint32,

@@ -284,13 +284,31 @@ class Context:
                 N.lib.epi_free(C.cast(ptr_, C.c_void_p))
         return off, s, e
 
-    def mine_raw(self, threshold: int, bins: Sequence, max_level: int, mode: int = N.MODE_MINE):
+    def mine_raw(self, threshold: int, bins: Sequence, max_level: int, mode: int = N.MODE_MINE,
+                 shard=None):
+        """Device-resident mine(). shard = (rank, world, min_shard, allgather)
+        runs epi_mine_sharded: allgather(send_ptr, recv_ptr, bytes_per_rank,
+        stream_ptr) -> 0 must all-gather the per-rank count slices (see
+        shard.make_allgather)."""
         lo = np.array([b[0] for b in bins], dtype=np.int64)
         hi = np.array([b[1] for b in bins], dtype=np.int64)
         cfg = N.MineConfig(int(threshold), int(max_level), N.ptr(lo, C.c_int64), N.ptr(hi, C.c_int64),
                            len(bins), int(mode))
         res = N.MineResult()
-        self._check(N.lib.epi_mine(self._h, C.byref(cfg), C.byref(res)))
+        if shard is None:
+            self._check(N.lib.epi_mine(self._h, C.byref(cfg), C.byref(res)))
+        else:
+            rank, world, min_shard, fn = shard
+
+            def _cb(user, send, recv, nbytes, stream):
+                try:
+                    return int(fn(send, recv, int(nbytes), stream) or 0)
+                except Exception as exc:  # noqa: BLE001 - reported as EPI_ENCCL
+                    self.shard_error = exc
+                    return 1
+            cb = N.ALLGATHER_FN(_cb)  # kept alive for the duration of the call
+            sh = N.Shard(int(rank), int(world), int(min_shard), cb, None)
+            self._check(N.lib.epi_mine_sharded(self._h, C.byref(cfg), C.byref(sh), C.byref(res)))
         nl = int(res.n_levels)
         cands = [int(res.level_candidates[i]) for i in range(nl)]
         offs = [int(res.level_offsets[i]) for i in range(nl + 1)]

@@ -172,7 +172,14 @@ epi_status epi_count_tracking(epi_ctx* ctx, const epi_episode_batch* batch, uint
 epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out) {
   if (!ctx || !cfg || !out) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);
-  return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out); });
+  return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out, nullptr); });
+}
+
+epi_status epi_mine_sharded(epi_ctx* ctx, const epi_mine_config* cfg, const epi_shard* shard,
+                            epi_mine_result* out) {
+  if (!ctx || !cfg || !shard || !out) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out, shard); });
 }
 
 epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,

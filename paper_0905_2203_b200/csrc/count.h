@@ -18,11 +18,13 @@ struct CountLaunch {
   uint32_t blk_words;      // words per bitmap block (a_pad * kRowStride)
   int32_t stages;          // shared-memory ring depth (0: read rows from global)
   int32_t n_tiles;
-  const int32_t* seg_g;    // P+1 segment tile bounds (device), multiples of 4
+  int32_t seg_len;         // segment q covers tiles [q*seg_len, min((q+1)*seg_len, seg_end))
+  int32_t seg_end;         // 4-aligned end of the tile range
   int32_t P;               // segments
   int32_t window_tiles;    // tiles processed before a segment for its window
   int32_t hist_words;      // wide path: history words per position (ceil(max high / 32))
-  uint32_t n_eps;          // episodes (all of length n_nodes)
+  uint32_t n_eps;          // episodes (all of length n_nodes); row stride of the records
+  const uint32_t* n_dev;   // non-null: the live episode count is *n_dev <= n_eps (device)
   const uint32_t* ep_types;  // [n_eps * N]
   const uint32_t* ep_win;    // [n_eps * (N-1)]: (low+1) | high << 16
   const uint32_t* ep_sigma;  // [n_eps]: sum of highs
@@ -47,8 +49,9 @@ void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 // Exact counts of single-node episodes (popcount of the type's bitmap).
 void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_blocks,
                        const uint32_t* types, uint32_t n_eps, uint64_t* counts, cudaStream_t st);
-// *out += sum_i hist[types[i]] (matched-pair work model of a launch).
-void launch_matched_pairs(const uint32_t* types, uint64_t count, const unsigned long long* hist,
-                          unsigned long long* out, cudaStream_t st);
+// *out += sum_i hist[types[i]] over i < count (or < *n_dev * per when
+// n_dev is set): the matched-pair work model of a launch.
+void launch_matched_pairs(const uint32_t* types, uint64_t count, const uint32_t* n_dev, uint32_t per,
+                          const unsigned long long* hist, unsigned long long* out, cudaStream_t st);
 
 }  // namespace epi

@@ -78,6 +78,15 @@ __device__ __forceinline__ EpParams<N> load_episode(const CountLaunch& p, uint32
   return ep;
 }
 
+__device__ __forceinline__ int32_t seg_bound(const CountLaunch& p, int q) {
+  const int64_t g = static_cast<int64_t>(q) * p.seg_len;
+  return g < p.seg_end ? static_cast<int32_t>(g) : p.seg_end;
+}
+
+__device__ __forceinline__ uint32_t live_eps(const CountLaunch& p) {
+  return p.n_dev ? *p.n_dev : p.n_eps;
+}
+
 __device__ __forceinline__ size_t occ_index(int32_t g, uint32_t type, uint32_t blk_words) {
   return static_cast<size_t>(g >> 5) * blk_words + type * kRowStride + (g & 31);
 }
@@ -358,10 +367,13 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   const int stages = p.stages;
 
   const int q = blockIdx.y;
+  const uint32_t n_live = live_eps(p);
+  // launches sized for an upper bound (device-side count): idle CTAs leave
+  if (blockIdx.x * kMachThreads >= n_live) return;
   const uint32_t e = blockIdx.x * kMachThreads + threadIdx.x;
-  const bool active = e < p.n_eps;
-  const int32_t gq = p.seg_g[q];
-  const int32_t gend = p.seg_g[q + 1];
+  const bool active = e < n_live;
+  const int32_t gq = seg_bound(p, q);
+  const int32_t gend = seg_bound(p, q + 1);
   const int32_t g0 = (gq - p.window_tiles > 0 ? gq - p.window_tiles : 0) & ~3;
 
   EpParams<N> ep = load_episode<N>(p, active ? e : 0);
@@ -474,7 +486,7 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
 template <int N, class Hist>
 __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= p.n_eps) return;
+  if (e >= live_eps(p)) return;
   const EpParams<N> ep = load_episode<N>(p, e);
   uint64_t total = 0;
   bool restart = false;
@@ -495,8 +507,8 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
         pf_last[j] = qq < p.P ? p.f_last[ix] : ~0ull;
       }
     }
-    const int32_t gq = p.seg_g[q];
-    const int32_t gn = p.seg_g[q + 1];
+    const int32_t gq = seg_bound(p, q);
+    const int32_t gn = seg_bound(p, q + 1);
     const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
     const uint32_t fcnt = pf_cnt[q % kPrefetch];
     const uint64_t flast = pf_last[q % kPrefetch];

@@ -77,6 +77,9 @@ Engine::Engine(int device) : device_(device) {
   EPI_CUDA(cudaEventCreate(&ev0_));
   EPI_CUDA(cudaEventCreate(&ev1_));
   EPI_CUDA(cudaEventCreate(&ev2_));
+  EPI_CUDA(cudaMalloc(&d_log_, kLogSlots * sizeof(uint32_t)));
+  EPI_CUDA(cudaMalloc(&d_acc_, 4 * sizeof(unsigned long long)));
+  EPI_CUDA(cudaMemset(d_acc_, 0, 4 * sizeof(unsigned long long)));
 }
 
 Engine::~Engine() {
@@ -85,7 +88,67 @@ Engine::~Engine() {
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
   if (ev2_) cudaEventDestroy(ev2_);
+  for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+  if (d_log_) cudaFree(d_log_);
+  if (d_acc_) cudaFree(d_acc_);
   if (st_) cudaStreamDestroy(st_);
+}
+
+// ---- deferred statistics -----------------------------------------------------
+
+void Engine::begin_op() {
+  ev_used_ = 0;
+  timed_.clear();
+  slot_counters_.clear();
+  log_used_ = 0;
+  EPI_CUDA(cudaMemsetAsync(d_acc_, 0, 4 * sizeof(unsigned long long), st_));
+}
+
+cudaEvent_t Engine::next_event() {
+  if (ev_used_ == ev_pool_.size()) {
+    cudaEvent_t e;
+    EPI_CUDA(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  return ev_pool_[ev_used_++];
+}
+
+int Engine::new_slot() {
+  if (log_used_ >= kLogSlots) throw Error(EPI_EUNSUPPORTED, "device statistics log exhausted");
+  return log_used_++;
+}
+
+void Engine::flush_stats(epi_stats& stats) {
+  const size_t nlog = static_cast<size_t>(log_used_);
+  char* h = static_cast<char*>(pin_small_.get(64 + nlog * sizeof(uint32_t)));
+  auto* acc = reinterpret_cast<unsigned long long*>(h);
+  auto* log = reinterpret_cast<uint32_t*>(h + 64);
+  EPI_CUDA(cudaMemcpyAsync(acc, d_acc_, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+  if (nlog) EPI_CUDA(cudaMemcpyAsync(log, d_log_, nlog * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaStreamSynchronize(st_));
+  stats.patches += acc[0];
+  stats.matched_pairs += acc[1];
+  stats.pruned += acc[2];
+  for (const SlotCounter& s : slot_counters_) *s.target += log[s.slot];
+  for (const Timed& t : timed_) {
+    float ms = 0, map_ms = 0;
+    EPI_CUDA(cudaEventElapsedTime(&ms, t.e0, t.e1));
+    const uint64_t live = t.live_slot >= 0 ? log[t.live_slot] : t.n_host;
+    stats.total_ms += ms;
+    if (t.ms_out) *t.ms_out += ms;
+    if (t.map) {
+      EPI_CUDA(cudaEventElapsedTime(&map_ms, t.e0, t.e_map));
+      stats.map_ms += map_ms;
+      stats.concat_ms += ms - map_ms;
+      stats.episode_events += live * stream_.n;
+      stats.tile_steps += live * t.tiles_per_ep;
+    }
+  }
+  timed_.clear();
+  slot_counters_.clear();
+  log_used_ = 0;
+  ev_used_ = 0;
+  EPI_CUDA(cudaMemsetAsync(d_acc_, 0, 4 * sizeof(unsigned long long), st_));
 }
 
 // Host -> device through pinned staging unless the source is already pinned.
@@ -208,29 +271,28 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
 }
 
 // Exact counts of a device-resident set into d_counts (device). Plans the
-// MapConcatenate segments, launches the map and concat-walk kernels, and
-// waits for them (stats need the patch counter and the event times).
-void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out) {
+// MapConcatenate segments and launches the map and concat-walk kernels; the
+// host does not wait (timings and counters are resolved by flush_stats).
+void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out,
+                          int live_slot) {
   const size_t n = ds.n;
   if (n == 0) return;
   const uint32_t N = ds.N;
+  const uint32_t* n_dev = live_slot >= 0 ? slot_ptr(live_slot) : nullptr;
   if (N == 1) {
+    if (n_dev) throw Error(EPI_EUNSUPPORTED, "single-node sets need a host-known size");
     // every distinct firing time is a completion: popcount of the bitmap
     const uint32_t n_blocks = static_cast<uint32_t>((stream_.n_tiles + kBlkTiles - 1) / kBlkTiles);
-    EPI_CUDA(cudaEventRecord(ev0_, st_));
+    Timed t{next_event(), nullptr, next_event(), ms_out, -1, n,
+            static_cast<uint64_t>(n_blocks) * kBlkTiles, true};
+    t.e_map = t.e1;
+    EPI_CUDA(cudaEventRecord(t.e0, st_));
     launch_singletons(stream_.d_occ, stream_.blk_words, n_blocks, ds.types, static_cast<uint32_t>(n),
                       d_counts, st_);
-    EPI_CUDA(cudaEventRecord(ev1_, st_));
-    EPI_CUDA(cudaEventSynchronize(ev1_));
-    float ms = 0;
-    EPI_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    EPI_CUDA(cudaEventRecord(t.e1, st_));
+    timed_.push_back(t);
     stats.kernel_launches += 1;
     stats.map_launches += 1;
-    stats.total_ms += ms;
-    stats.map_ms += ms;
-    stats.episode_events += static_cast<uint64_t>(n) * stream_.n;
-    stats.tile_steps += static_cast<uint64_t>(n) * n_blocks * kBlkTiles;
-    if (ms_out) *ms_out += ms;
     return;
   }
   // Wide windows need a bitmap whose gap compression cap exceeds them, and
@@ -245,6 +307,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   p.stages = stages_for(stream_.blk_words);
   p.hist_words = hist_words;
   p.n_eps = static_cast<uint32_t>(n);
+  p.n_dev = n_dev;
   p.ep_types = ds.types;
   p.ep_win = ds.win;
   p.ep_sigma = ds.sigma;
@@ -258,19 +321,33 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
 
   // MapConcatenate plan. Segments must each span sum(high) (the window of a
   // segment lies inside its predecessor). Cost model in tile steps of one
-  // thread: waves(P) * (tiles/P + window) for the map kernel (waves = map
-  // CTAs over resident CTA slots) plus kWalkStep per segment for the
-  // sequential concat walk; P = 1 needs no walk at all.
+  // thread, calibrated on the B200 (scripts/seg_sweep.py): the map kernel is
+  // ALU-bound, so co-resident CTAs share an SM's issue rate and an SM's time
+  // is the number of CTAs it receives times their length,
+  // ceil(CTAs / SMs) * (tiles/P + window), inflated when the grid cannot
+  // fill the resident slots (latency no longer hidden); plus kWalkStep per
+  // segment for the sequential concat walk. P = 1 needs no walk at all.
   const int64_t n_tiles = static_cast<int64_t>(stream_.n_tiles);
   const int64_t tiles4 = (n_tiles + 3) / 4 * 4;
   const uint32_t max_sigma = ds.max_sigma;
   const int32_t window_tiles = static_cast<int32_t>((max_sigma + 31) / 32 + 1);
   constexpr int64_t kMaxWalkSegments = 128;
   constexpr double kWalkStep = 20.0;
-  int bps = 1;
-  p.occ_query = &bps;
-  launch_map();
-  p.occ_query = nullptr;
+  // resident map CTAs per SM for this launch shape (cached per shape)
+  const uint64_t shape = (static_cast<uint64_t>(N) << 48) ^ (static_cast<uint64_t>(ds.width) << 40) ^
+                         (static_cast<uint64_t>(ds.max_high <= 32) << 39) ^
+                         (static_cast<uint64_t>(wide) << 38) ^
+                         (static_cast<uint64_t>(p.stages) << 32) ^ p.blk_words;
+  int bps = 0;
+  for (const auto& kv : occ_cache_)
+    if (kv.first == shape) bps = kv.second;
+  if (bps == 0) {
+    bps = 1;
+    p.occ_query = &bps;
+    launch_map();
+    p.occ_query = nullptr;
+    occ_cache_.emplace_back(shape, bps);
+  }
   const int64_t slots = static_cast<int64_t>(num_sms_) * bps;
   const int64_t ctas_x = (static_cast<int64_t>(n) + 255) / 256;
   const int64_t min_seg = std::max<int64_t>(window_tiles * 4, 32);
@@ -278,9 +355,11 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   int64_t P = 1;
   double best = 1e300;
   for (int64_t cand = 1; cand <= max_p; ++cand) {
-    const double waves = static_cast<double>((ctas_x * cand + slots - 1) / slots);
+    const int64_t ctas = ctas_x * cand;
+    const double rounds = static_cast<double>((ctas + num_sms_ - 1) / num_sms_);
+    const double fill = std::min(1.0, static_cast<double>(ctas) / static_cast<double>(slots));
     const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
-    const double cost = waves * per + (cand > 1 ? kWalkStep * cand : 0.0);
+    const double cost = rounds * per * (1.0 + 0.3 * (1.0 - fill)) + (cand > 1 ? kWalkStep * cand : 0.0);
     if (cost < best * 0.999) {
       best = cost;
       P = cand;
@@ -298,62 +377,44 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // bitmap is zero past the stream).
   const int64_t seg_len = ((tiles4 + P - 1) / P + 3) / 4 * 4;
   P = (tiles4 + seg_len - 1) / seg_len;
-  int32_t* h_seg = static_cast<int32_t*>(pin_seg_.get((P + 1) * sizeof(int32_t)));
-  for (int64_t q = 0; q < P; ++q) h_seg[q] = static_cast<int32_t>(q * seg_len);
-  h_seg[P] = static_cast<int32_t>(tiles4);
-  int32_t* d_seg = scratch_.get<int32_t>(kSlotSegments, P + 1 + 6);
-  EPI_CUDA(cudaMemcpyAsync(d_seg, h_seg, (P + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
-  unsigned long long* d_patch = reinterpret_cast<unsigned long long*>(d_seg + ((P + 2) & ~1));
-  EPI_CUDA(cudaMemsetAsync(d_patch, 0, 2 * sizeof(unsigned long long), st_));
   // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k).
-  launch_matched_pairs(ds.types, n * N, stream_.d_hist, d_patch + 1, st_);
+  launch_matched_pairs(ds.types, n * N, n_dev, N, stream_.d_hist, d_acc_ + 1, st_);
 
   const size_t nm = P > 1 ? static_cast<size_t>(P) * n : 1;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
                m_first = align_up(m_last + nm * 8, 256), m_total = m_first + nm * 8 * kRecorded;
   char* d_mach = scratch_.get<char>(kSlotMachines, m_total);
   p.n_tiles = static_cast<int32_t>(n_tiles);
-  p.seg_g = d_seg;
+  p.seg_len = static_cast<int32_t>(seg_len);
+  p.seg_end = static_cast<int32_t>(tiles4);
   p.P = static_cast<int32_t>(P);
   p.window_tiles = window_tiles;
   p.f_count = reinterpret_cast<uint32_t*>(d_mach + m_count);
   p.f_ncomp = reinterpret_cast<uint32_t*>(d_mach + m_ncomp);
   p.f_last = reinterpret_cast<uint64_t*>(d_mach + m_last);
   p.f_first = reinterpret_cast<uint64_t*>(d_mach + m_first);
-  p.patches = d_patch;
+  p.patches = d_acc_;
 
-  EPI_CUDA(cudaEventRecord(ev0_, st_));
+  uint64_t tiles = 0;
+  for (int64_t q = 0; q < P; ++q) {
+    const int64_t gq = q * seg_len, gn = std::min<int64_t>((q + 1) * seg_len, tiles4);
+    tiles += static_cast<uint64_t>(gn - std::max<int64_t>(gq - window_tiles, 0));
+  }
+  Timed t{next_event(), next_event(), next_event(), ms_out, live_slot, n, tiles, true};
+  EPI_CUDA(cudaEventRecord(t.e0, st_));
   launch_map();
-  EPI_CUDA(cudaEventRecord(ev2_, st_));
+  EPI_CUDA(cudaEventRecord(t.e_map, st_));
   if (P > 1) {
     if (wide)
       launch_walk_wide(static_cast<int>(N), p, st_);
     else
       launch_walk(static_cast<int>(N), p, st_);
   }
-  EPI_CUDA(cudaEventRecord(ev1_, st_));
-  unsigned long long* h_patch = static_cast<unsigned long long*>(pin_small_.get(64)) + 4;
-  EPI_CUDA(cudaMemcpyAsync(h_patch, d_patch, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                           st_));
-  EPI_CUDA(cudaStreamSynchronize(st_));
-  float ms = 0, map_ms = 0;
-  EPI_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
-  EPI_CUDA(cudaEventElapsedTime(&map_ms, ev0_, ev2_));
-  stats.patches += h_patch[0];
+  EPI_CUDA(cudaEventRecord(t.e1, st_));
+  timed_.push_back(t);
   stats.segments = static_cast<uint64_t>(P);
   stats.kernel_launches += P > 1 ? 3 : 2;  // matched-pair stats + map (+ walk)
   stats.map_launches += 1;
-  stats.total_ms += ms;
-  stats.map_ms += map_ms;
-  stats.concat_ms += ms - map_ms;
-  stats.h2d_bytes += (P + 1) * sizeof(int32_t);
-  stats.episode_events += static_cast<uint64_t>(n) * stream_.n;
-  stats.matched_pairs += h_patch[1];
-  uint64_t tiles = 0;
-  for (int64_t q = 0; q < P; ++q)
-    tiles += static_cast<uint64_t>(h_seg[q + 1] - std::max<int64_t>(h_seg[q] - window_tiles, 0));
-  stats.tile_steps += tiles * n;
-  if (ms_out) *ms_out += ms;
 }
 
 void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
@@ -450,6 +511,7 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
   epi_stats stats{};
   const uint64_t n = b.n_episodes;
   if (n && (!b.offsets || !counts_out)) throw Error(EPI_EINVAL, "epi_count: null batch arrays");
+  begin_op();
   if (mode > EPI_MODE_MINE) throw Error(EPI_EINVAL, "epi_count: unknown mode");
   // validate(Episode) for every candidate first (E/types.hpp:87-92).
   std::vector<uint32_t> lens(n);
@@ -484,6 +546,7 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
   if (frequent_out)
     for (uint64_t e = 0; e < n; ++e)
       frequent_out[e] = counts_out[e] != kPruned && counts_out[e] >= threshold;
+  flush_stats(stats);
   if (stats_out) *stats_out = stats;
 }
 

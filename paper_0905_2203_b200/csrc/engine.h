@@ -40,6 +40,27 @@ struct DevSet {
   int width = 0;                    // launch-uniform high-low, 0 if mixed
 };
 
+// Host memory the device writes directly (zero-copy): small, sparse outputs
+// such as a level's frequent episodes arrive without a sized D2H copy.
+struct MappedBuffer {
+  void* p = nullptr;
+  void* d = nullptr;
+  size_t bytes = 0;
+  ~MappedBuffer() {
+    if (p) cudaFreeHost(p);
+  }
+  void get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      size_t grow = need + need / 4 + 4096;
+      EPI_CUDA(cudaHostAlloc(&p, grow, cudaHostAllocMapped));
+      EPI_CUDA(cudaHostGetDevicePointer(&d, p, 0));
+      bytes = grow;
+    }
+  }
+};
+
 struct PinnedBuffer {
   void* p = nullptr;
   size_t bytes = 0;
@@ -76,7 +97,8 @@ class Engine {
   // Arbitrary CSR batch (mixed lengths): validated, grouped by length.
   void count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
                    uint64_t* counts_out, uint8_t* frequent_out, epi_stats* stats);
-  void mine(const epi_mine_config& cfg, epi_mine_result* out);
+  // shard == nullptr: single device (epi_mine); else epi_mine_sharded.
+  void mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_shard* shard);
   // Parallel local tracking (tracking.cu): counts (greedy) and/or intervals.
   void track_batch(const epi_episode_batch& b, uint32_t direction, uint64_t* counts_out,
                    std::vector<uint64_t>* off_out, std::vector<int64_t>* starts,
@@ -89,13 +111,48 @@ class Engine {
   // Exact count of one fixed-length set on the device.
   void count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                    double* ms_out);
-  void count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out);
+  // Launches only: timings and counters are resolved by flush_stats.
+  // live_slot >= 0: ds.n is an upper bound and the live count is the
+  // device log value log_[live_slot] (written by an earlier kernel).
+  void count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats, double* ms_out,
+                    int live_slot = -1);
   // uniform_win != 0: pass-1 relaxation uses that window at every position.
   void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
                              uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats);
-  uint32_t dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n,
-                              const unsigned long long* extra = nullptr,
-                              unsigned long long* extra_out = nullptr);
+  // Exclusive scan of n u32 flags; the total goes to device log slot `slot`
+  // (and to *host_total, zero-copy, when given). No host synchronisation.
+  void dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, int slot,
+                      uint32_t* host_total = nullptr);
+
+  // ---- deferred statistics: no host sync per launch ------------------------
+  // begin_op resets the per-call state; flush_stats synchronises once and
+  // resolves every recorded interval and device counter into `stats`.
+  void begin_op();
+  void flush_stats(epi_stats& stats);
+  cudaEvent_t next_event();
+  int new_slot();  // a device u32 log slot, unique within the call
+  uint32_t* slot_ptr(int s) { return d_log_ + s; }
+  struct Timed {
+    cudaEvent_t e0, e_map, e1;
+    double* ms_out;
+    int live_slot;        // -1: n_host episodes
+    uint64_t n_host;
+    uint64_t tiles_per_ep;
+    bool map;             // automaton launch (map_ms / concat_ms split)
+  };
+  struct SlotCounter {
+    int slot;
+    uint64_t* target;
+  };
+  std::vector<cudaEvent_t> ev_pool_;
+  size_t ev_used_ = 0;
+  std::vector<Timed> timed_;
+  std::vector<SlotCounter> slot_counters_;
+  uint32_t* d_log_ = nullptr;            // kLogSlots u32
+  unsigned long long* d_acc_ = nullptr;  // [0] patches [1] matched pairs [2] pruned
+  int log_used_ = 0;
+  static constexpr int kLogSlots = 4096;
+  std::vector<std::pair<uint64_t, int>> occ_cache_;  // (launch shape key, CTAs/SM)
   void h2d(void* dst, const void* src, size_t bytes);
   void ensure_type_index();
 
@@ -112,7 +169,8 @@ class Engine {
   cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, ev2_ = nullptr;
   DeviceStream stream_;
   DeviceScratch scratch_;
-  PinnedBuffer pin_up_, pin_down_, pin_seg_, pin_small_;
+  PinnedBuffer pin_up_, pin_down_, pin_small_;
+  MappedBuffer map_out_, map_small_;
 
   // epi_mine result storage
   std::vector<uint64_t> m_level_cands_, m_level_off_, m_counts_;

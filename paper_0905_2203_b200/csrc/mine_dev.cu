@@ -47,8 +47,7 @@ enum MineSlot : size_t {
   kMGroupCnt,
   kMSurv,      // survivor params
   kMSurvCnt,
-  kMOut,       // compacted frequent output
-  kMPruned,
+  kMGather,    // all-gathered level counts (sharded mining)
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -197,9 +196,18 @@ __global__ void gather_kernel(const uint32_t* __restrict__ flags, const uint32_t
 }
 
 __global__ void scatter_counts_kernel(const uint32_t* __restrict__ oidx, const uint64_t* __restrict__ c,
-                                      uint32_t m, uint64_t* counts) {
+                                      const uint32_t* __restrict__ m_dev, uint64_t* counts) {
   const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o < m) counts[oidx[o]] = c[o];
+  if (o < *m_dev) counts[oidx[o]] = c[o];
+}
+
+// total of an exclusive scan = scan[n-1] + flags[n-1] -> device log slot
+// (and a zero-copy host word when given)
+__global__ void scan_total_kernel(const uint32_t* __restrict__ scan, const uint32_t* __restrict__ flags,
+                                  uint64_t n, uint32_t* slot, uint32_t* host) {
+  const uint32_t t = scan[n - 1] + flags[n - 1];
+  *slot = t;
+  if (host) *reinterpret_cast<volatile uint32_t*>(host) = t;
 }
 
 __global__ void freq_flags_kernel(const uint64_t* __restrict__ counts, uint64_t threshold, uint64_t n,
@@ -228,25 +236,22 @@ inline unsigned blocks_for(uint64_t n, unsigned t = 256) {
 
 }  // namespace
 
-// Exclusive scan of n u32 flags into scan[]; returns the total.
-// One stream sync returns the total (and, optionally, one more device u64).
-uint32_t Engine::dev_exclusive_scan(const uint32_t* flags, uint32_t* scan, uint64_t n,
-                                    const unsigned long long* extra, unsigned long long* extra_out) {
+// Exclusive scan of n u32 flags into scan[]; the total lands in device log
+// slot `slot` (and in *host_total, zero-copy). No host synchronisation.
+void Engine::dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, int slot,
+                            uint32_t* host_total) {
   size_t tmp = 0;
   EPI_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flags, scan, static_cast<int>(n), st_));
   void* d_tmp = scratch_.get<char>(kMCub, tmp + 16);
   EPI_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp, flags, scan, static_cast<int>(n), st_));
-  uint32_t* h = static_cast<uint32_t*>(pin_small_.get(32));
-  EPI_CUDA(cudaMemcpyAsync(h, scan + n - 1, 4, cudaMemcpyDeviceToHost, st_));
-  EPI_CUDA(cudaMemcpyAsync(h + 1, flags + n - 1, 4, cudaMemcpyDeviceToHost, st_));
-  if (extra) EPI_CUDA(cudaMemcpyAsync(h + 2, extra, 8, cudaMemcpyDeviceToHost, st_));
-  EPI_CUDA(cudaStreamSynchronize(st_));
-  if (extra_out) std::memcpy(extra_out, h + 2, 8);
-  return h[0] + h[1];
+  scan_total_kernel<<<1, 1, 0, st_>>>(scan, flags, n, slot_ptr(slot), host_total);
+  EPI_CUDA(cudaGetLastError());
 }
 
 // Counts of the device-resident candidate set `c` into d_counts: exact, or
-// two-pass (MINE) with PRUNED sentinels for eliminated candidates.
+// two-pass (MINE) with PRUNED sentinels for eliminated candidates. One host
+// synchronisation (the group count decides whether pass 1 pays); survivors
+// are sized on the device.
 void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
                                    uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats) {
   const uint64_t n = c.n;
@@ -286,8 +291,12 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
   head_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(skeys, n, flags);
   EPI_CUDA(cudaGetLastError());
-  const uint32_t n_groups = dev_exclusive_scan(flags, scan, n);
-  stats.kernel_launches += 4;
+  map_small_.get(64);
+  uint32_t* h_groups = static_cast<uint32_t*>(map_small_.p);
+  dev_scan_total(flags, scan, n, new_slot(), h_groups);
+  EPI_CUDA(cudaStreamSynchronize(st_));
+  const uint32_t n_groups = *reinterpret_cast<volatile uint32_t*>(h_groups);
+  stats.kernel_launches += 5;
   if (2ull * n_groups > n) {
     // type sequences barely repeat: relaxed counts would cost as much as
     // the exact ones, so count everything exactly
@@ -326,49 +335,51 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
 
   // Survivor flags go to the index buffer the sort left free.
   uint32_t* sflags = sidx == idx ? idx_alt : idx;
-  unsigned long long* d_pruned = reinterpret_cast<unsigned long long*>(scratch_.get<char>(kMPruned, 16));
-  EPI_CUDA(cudaMemsetAsync(d_pruned, 0, 8, st_));
   // A singleton group's per-group hull is the episode itself (exact); the
   // uniform alphabet hull is only a bound.
   prune_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx, flags, scan, gsize, bound, threshold, n,
-                                               uniform_win == 0, d_counts, sflags, d_pruned);
+                                               uniform_win == 0, d_counts, sflags, d_acc_ + 2);
   EPI_CUDA(cudaGetLastError());
   uint32_t* sscan = scan;
-  unsigned long long pruned = 0;
-  const uint32_t m = dev_exclusive_scan(sflags, sscan, n, d_pruned, &pruned);
-  stats.pruned += pruned;
+  const int mslot = new_slot();
+  dev_scan_total(sflags, sscan, n, mslot);
+  slot_counters_.push_back({mslot, &stats.pass2_episodes});
+  stats.kernel_launches += 4;
+  // Survivors (m <= n, known only on the device): buffers and grids sized
+  // for n, kernels read m from the log slot.
+  const size_t s_types = 0, s_win = align256(static_cast<size_t>(n) * L * 4),
+               s_sigma = s_win + align256(static_cast<size_t>(n) * M * 4),
+               s_idx = s_sigma + align256(n * 4ull), s_total = s_idx + align256(n * 4ull);
+  char* sbuf = scratch_.get<char>(kMSurv, s_total);
+  uint32_t* stypes = reinterpret_cast<uint32_t*>(sbuf + s_types);
+  uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
+  uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
+  uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
+  gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
+                                                swin, ssigma, sidx_out);
+  EPI_CUDA(cudaGetLastError());
+  DevSet sv = c;
+  sv.n = n;
+  sv.types = stypes;
+  sv.win = swin;
+  sv.sigma = ssigma;
+  uint64_t* sc = scratch_.get<uint64_t>(kMSurvCnt, n);
+  count_device(sv, sc, stats, &stats.pass2_ms, mslot);
+  scatter_counts_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx_out, sc, slot_ptr(mslot), d_counts);
+  EPI_CUDA(cudaGetLastError());
   stats.kernel_launches += 2;
-  stats.pass2_episodes += m;
-  if (m > 0) {
-    const size_t s_types = 0, s_win = align256(static_cast<size_t>(m) * L * 4),
-                 s_sigma = s_win + align256(static_cast<size_t>(m) * M * 4),
-                 s_idx = s_sigma + align256(m * 4ull), s_total = s_idx + align256(m * 4ull);
-    char* sbuf = scratch_.get<char>(kMSurv, s_total);
-    uint32_t* stypes = reinterpret_cast<uint32_t*>(sbuf + s_types);
-    uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
-    uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
-    uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
-    gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
-                                                  swin, ssigma, sidx_out);
-    EPI_CUDA(cudaGetLastError());
-    DevSet sv = c;
-    sv.n = m;
-    sv.types = stypes;
-    sv.win = swin;
-    sv.sigma = ssigma;
-    uint64_t* sc = scratch_.get<uint64_t>(kMSurvCnt, m);
-    count_device(sv, sc, stats, &stats.pass2_ms);
-    scatter_counts_kernel<<<blocks_for(m), 256, 0, st_>>>(sidx_out, sc, m, d_counts);
-    EPI_CUDA(cudaGetLastError());
-    stats.kernel_launches += 2;
-  }
 }
 
-// mine (E/miner.hpp:114-173), device-resident.
-void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
+// mine (E/miner.hpp:114-173), device-resident; with `shard`, each large
+// level's counting is split over the ranks and re-assembled by the caller's
+// all-gather (epi_mine_sharded).
+void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_shard* shard) {
   if (cfg.threshold < 1) throw Error(EPI_EINVAL, "mine: threshold must be >= 1");
   if (cfg.max_level < 1) throw Error(EPI_EINVAL, "mine: max_level must be >= 1");
   if (cfg.n_alpha == 0) throw Error(EPI_EINVAL, "mine: constraint alphabet must not be empty");
+  const uint32_t W = shard ? shard->world : 1, R = shard ? shard->rank : 0;
+  if (shard && (W == 0 || R >= W || (W > 1 && !shard->allgather)))
+    throw Error(EPI_EINVAL, "mine: invalid shard (rank, world, allgather)");
   std::vector<uint32_t> awin(cfg.n_alpha), ahi(cfg.n_alpha);
   int64_t amax = 0, amin_lo = INT64_MAX;
   int awidth = -1;
@@ -395,8 +406,8 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
   m_lo_.clear();
   m_hi_.clear();
   epi_stats totals{};
+  begin_op();
   const uint32_t A = stream_.alphabet;
-  const std::vector<uint64_t>& hist = stream_.type_hist;
 
   // Frequent set of the previous level, host side (types, packed windows).
   std::vector<uint32_t> ftypes, fwin;
@@ -448,14 +459,10 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
 
     // ---- candidate generation on the device ----------------------------
     uint64_t n = 0;
-    uint64_t matched = 0;
     std::vector<uint32_t> pre, lrange;
     std::vector<uint64_t> loff;
     if (level == 2) {
       n = static_cast<uint64_t>(nf) * nf * cfg.n_alpha;
-      uint64_t hsum = 0;
-      for (uint32_t t : ftypes) hsum += hist[t];
-      matched = 2ull * cfg.n_alpha * nf * hsum;
     } else {
       // Join index over the frequent set: stable sort by the prefix key
       // (first L-2 nodes + their constraints), exact comparisons.
@@ -477,10 +484,6 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
       std::iota(pre.begin(), pre.end(), 0u);
       std::stable_sort(pre.begin(), pre.end(),
                        [&](uint32_t a, uint32_t b) { return cmp_key(a, 0, b, 0) < 0; });
-      // prefix sums of hist[last type] in sorted order (matched-pair stats)
-      std::vector<uint64_t> hlast(nf + 1, 0);
-      for (size_t b = 0; b < nf; ++b)
-        hlast[b + 1] = hlast[b] + hist[ftypes[static_cast<size_t>(pre[b]) * F + F - 1]];
       lrange.resize(2 * nf);
       loff.assign(nf + 1, 0);
       for (uint32_t l = 0; l < nf; ++l) {
@@ -494,19 +497,22 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
         lrange[2 * l] = b0;
         lrange[2 * l + 1] = b1;
         loff[l + 1] = loff[l] + (b1 - b0);
-        uint64_t ml = 0;
-        for (uint32_t k = 0; k < F; ++k) ml += hist[ftypes[static_cast<size_t>(l) * F + k]];
-        matched += ml * (b1 - b0) + (hlast[b1] - hlast[b0]);
       }
       n = loff[nf];
     }
     if (n == 0) break;
     if (n >= (1ull << 31)) throw Error(EPI_EUNSUPPORTED, "more than 2^31 candidates in one level");
 
+    // Sharding of this level: rank R counts [R*s, R*s + cnt) of s-wide slices.
+    const bool sharded = W > 1 && n >= std::max<uint64_t>(shard->min_shard, static_cast<uint64_t>(W) * W);
+    const uint64_t s = sharded ? (n + W - 1) / W : n;
+    const uint64_t lo_c = sharded ? std::min<uint64_t>(static_cast<uint64_t>(R) * s, n) : 0;
+    const uint64_t cnt_c = sharded ? std::min<uint64_t>(s, n - lo_c) : n;
+
     uint32_t* d_types = scratch_.get<uint32_t>(kMTypes, n * L);
     uint32_t* d_win = scratch_.get<uint32_t>(kMWin, n * (L - 1));
     uint32_t* d_sigma = scratch_.get<uint32_t>(kMSigma, n);
-    uint64_t* d_counts = scratch_.get<uint64_t>(kMCounts, n);
+    uint64_t* d_counts = scratch_.get<uint64_t>(kMCounts, sharded ? s * W : n);
     if (level == 2) {
       const size_t up = nf + 2 * cfg.n_alpha;
       uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up * 4));
@@ -531,9 +537,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
       std::memcpy(h + o_w, fwin.data(), nf * (F - 1) * 4);
       uint32_t* hs = reinterpret_cast<uint32_t*>(h + o_s);
       for (size_t i = 0; i < nf; ++i) {
-        uint32_t s = 0;
-        for (uint32_t k = 0; k + 1 < F; ++k) s += fwin[i * (F - 1) + k] >> 16;
-        hs[i] = s;
+        uint32_t sg = 0;
+        for (uint32_t k = 0; k + 1 < F; ++k) sg += fwin[i * (F - 1) + k] >> 16;
+        hs[i] = sg;
       }
       std::memcpy(h + o_p, pre.data(), nf * 4);
       std::memcpy(h + o_r, lrange.data(), nf * 8);
@@ -553,42 +559,49 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
 
     DevSet c;
     c.N = L;
-    c.n = n;
-    c.types = d_types;
-    c.win = d_win;
-    c.sigma = d_sigma;
+    c.n = cnt_c;
+    c.types = d_types + lo_c * L;
+    c.win = d_win + lo_c * (L - 1);
+    c.sigma = d_sigma + lo_c;
     c.max_high = amax;
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
-    count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, d_counts, totals);
+    if (cnt_c > 0) count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, d_counts + lo_c, totals);
+    if (sharded) {
+      // every rank's s-wide slice -> the full count vector in candidate order
+      uint64_t* d_all = scratch_.get<uint64_t>(kMGather, s * W);
+      const int rc = shard->allgather(shard->user, d_counts + static_cast<uint64_t>(R) * s, d_all,
+                                      s * sizeof(uint64_t), static_cast<void*>(st_));
+      if (rc != 0) throw Error(EPI_ENCCL, "mine: all-gather of level counts failed");
+      d_counts = d_all;
+    }
 
-    // ---- threshold + compaction in candidate order ------------------------
+    // ---- threshold + compaction in candidate order, straight to host -----
     uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
     uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
     freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(d_counts, cfg.threshold, n, flags);
     EPI_CUDA(cudaGetLastError());
-    const uint32_t k = dev_exclusive_scan(flags, scan, n);
-    totals.kernel_launches += 2;
+    map_small_.get(64);
+    uint32_t* h_k = static_cast<uint32_t*>(map_small_.p) + 1;
+    dev_scan_total(flags, scan, n, new_slot(), h_k);
+    const size_t o_t = 0, o_w = align256(static_cast<size_t>(n) * L * 4),
+                 o_c = o_w + align256(static_cast<size_t>(n) * (L - 1) * 4), o_end = o_c + align256(n * 8ull);
+    map_out_.get(o_end);
+    char* dm = static_cast<char*>(map_out_.d);
+    compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
+        flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(dm + o_t),
+        reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c));
+    EPI_CUDA(cudaGetLastError());
+    EPI_CUDA(cudaStreamSynchronize(st_));
+    totals.kernel_launches += 5;
+    const uint32_t k = *reinterpret_cast<volatile uint32_t*>(h_k);
+    const char* hm = static_cast<const char*>(map_out_.p);
     std::vector<uint32_t> ntypes(static_cast<size_t>(k) * L), nwin(static_cast<size_t>(k) * (L - 1));
     std::vector<uint64_t> ncnt(k);
-    if (k > 0) {
-      const size_t o_t = 0, o_w = align256(static_cast<size_t>(k) * L * 4),
-                   o_c = o_w + align256(static_cast<size_t>(k) * (L - 1) * 4),
-                   o_end = o_c + align256(k * 8ull);
-      char* d = scratch_.get<char>(kMOut, o_end);
-      compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
-          flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(d + o_t),
-          reinterpret_cast<uint32_t*>(d + o_w), reinterpret_cast<uint64_t*>(d + o_c));
-      EPI_CUDA(cudaGetLastError());
-      char* h = static_cast<char*>(pin_down_.get(o_end));
-      EPI_CUDA(cudaMemcpyAsync(h, d, o_end, cudaMemcpyDeviceToHost, st_));
-      EPI_CUDA(cudaStreamSynchronize(st_));
-      totals.d2h_bytes += o_end;
-      totals.kernel_launches += 1;
-      std::memcpy(ntypes.data(), h + o_t, ntypes.size() * 4);
-      std::memcpy(nwin.data(), h + o_w, nwin.size() * 4);
-      std::memcpy(ncnt.data(), h + o_c, ncnt.size() * 8);
-    }
+    std::memcpy(ntypes.data(), hm + o_t, ntypes.size() * 4);
+    std::memcpy(nwin.data(), hm + o_w, nwin.size() * 4);
+    std::memcpy(ncnt.data(), hm + o_c, ncnt.size() * 8);
+    totals.d2h_bytes += static_cast<uint64_t>(k) * (8 + 4 * (2 * L - 1)) + 4;
     record_level(n, L, ntypes.data(), nwin.data(), ncnt.data(), k,
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     ftypes.swap(ntypes);
@@ -597,6 +610,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out) {
     nf = k;
     if (nf == 0) break;
   }
+  flush_stats(totals);
   out->n_levels = m_level_cands_.size();
   out->level_candidates = m_level_cands_.data();
   out->level_offsets = m_level_off_.data();

@@ -13,6 +13,7 @@ The counting function is injected: the product passes the device counter
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Callable, Sequence
 
 import numpy as np
@@ -58,6 +59,56 @@ def count_sharded(csr: CSR, count_fn: Callable, group=None, device=None, thresho
     lo, hi = shard_bounds(n, world, rank)
     local = count_fn(slice_csr(csr, lo, hi), threshold, mode) if hi > lo else np.zeros(0, np.uint64)
     return allgather_counts(np.asarray(local, dtype=np.uint64), n, group, device)
+
+
+class _RawDevice:
+    """A device byte range as a __cuda_array_interface__ object (zero-copy
+    torch view of an engine buffer)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def make_allgather(group=None, memory: str = "cuda", device=None):
+    """The all-gather callback of epi_mine_sharded (Context.mine_raw(shard=...)).
+
+    memory="cuda":   the pointers are device buffers on the engine's stream;
+                     NCCL all_gather_into_tensor enqueued on that stream
+                     (torch.cuda.ExternalStream), no host round trip.
+    memory="staged": device buffers, gathered through host copies (gloo;
+                     functional runs of several ranks on one GPU).
+    memory="host":   the pointers are host memory (CPU tests of the plumbing).
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+
+    def host_view(ptr, nbytes):
+        return torch.from_numpy(np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(int(ptr))))
+
+    def fn(send, recv, nbytes, stream):
+        if memory == "host":
+            src = host_view(send, nbytes)
+            parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, src.clone(), group=group)
+            host_view(recv, nbytes * world).copy_(torch.cat(parts))
+            return 0
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        s = torch.cuda.ExternalStream(int(stream), device=dev)
+        with torch.cuda.stream(s):
+            src = torch.as_tensor(_RawDevice(send, nbytes), device=dev)
+            dst = torch.as_tensor(_RawDevice(recv, nbytes * world), device=dev)
+            if memory == "cuda":
+                dist.all_gather_into_tensor(dst, src, group=group)
+            else:
+                h = src.cpu()
+                parts = [torch.empty_like(h) for _ in range(world)]
+                dist.all_gather(parts, h, group=group)
+                dst.copy_(torch.cat(parts))
+                s.synchronize()
+        return 0
+    return fn
 
 
 def mine_sharded(alphabet_size: int, threshold: int, bins: Sequence, max_level: int,

@@ -38,7 +38,18 @@ def _worker(rank, world, port, queue, task):
     try:
         import oracle
         from paper_0905_2203_b200.shard import count_sharded, mine_sharded, shard_bounds
-        if task == "count":
+        if task == "allgather":
+            # the epi_mine_sharded callback contract on host memory: send = this
+            # rank's s u64, recv = world * s u64 in rank order
+            from paper_0905_2203_b200.shard import make_allgather
+            s = 37
+            send = (np.arange(s, dtype=np.uint64) + 1000 * rank).astype(np.uint64)
+            recv = np.zeros(s * world, dtype=np.uint64)
+            fn = make_allgather(memory="host")
+            rc = fn(send.ctypes.data, recv.ctypes.data, s * 8, 0)
+            want = np.concatenate([np.arange(s, dtype=np.uint64) + 1000 * r for r in range(world)])
+            queue.put((rank, rc == 0 and bool(np.array_equal(recv, want)), True))
+        elif task == "count":
             rng = np.random.default_rng(3)
             times = np.cumsum(rng.integers(0, 5, 4000)).astype(np.int64)
             types = rng.integers(0, 6, 4000).astype(np.uint32)
@@ -83,6 +94,11 @@ def _run(task, world=2):
         p.join(timeout=60)
         assert p.exitcode == 0
     return sorted(out)
+
+
+def test_allgather_callback_world2():
+    for rank, ok, _ in _run("allgather"):
+        assert ok, rank
 
 
 def test_sharded_count_world2():
