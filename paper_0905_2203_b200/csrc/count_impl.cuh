@@ -104,7 +104,27 @@ template <int W, bool kHi32>
 __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t h2, uint32_t lo1,
                                                uint32_t hi) {
   uint32_t zl, zh;
-  if constexpr (kHi32 && W > 0) {
+  if constexpr (kHi32 && W >= 9) {
+    // wide uniform windows (e.g. the pass-1 hull of a bin alphabet): a
+    // compile-time doubling smear over Z = (c : h1) >> (32 - hi) costs
+    // ~2 log2(W) + 2 shifts instead of W (the high word is dropped after
+    // the last step)
+    const uint32_t s = 32u - hi;
+    uint32_t rl = __funnelshift_r(h1, c, s), rh = c >> s;
+    constexpr int kS1 = 1, kS2 = 2, kS3 = W - 4 < 4 ? W - 4 : 4;  // cover 1 -> 2 -> 4 -> 4 + kS3
+    rl |= __funnelshift_r(rl, rh, kS1);
+    rh |= rh >> kS1;
+    rl |= __funnelshift_r(rl, rh, kS2);
+    rh |= rh >> kS2;
+    if constexpr (W - 4 - kS3 > 0) {
+      rl |= __funnelshift_r(rl, rh, kS3);
+      rh |= rh >> kS3;
+      rl |= __funnelshift_r(rl, rh, W - 4 - kS3);  // cover 8 -> W (W <= 16)
+    } else {
+      rl |= __funnelshift_r(rl, rh, kS3);
+    }
+    return rl;
+  } else if constexpr (kHi32 && W > 0) {
     // X = (c : h1); term b of the smear is (c : h1) >> (32 - hi + b), and
     // 32 - hi + b <= 32 - lo1 <= 31, so each term is one funnel shift (ALU
     // pipe). (Moving terms to the FMA pipe as hi32(h1*m + ((c*m) << 32))
@@ -432,7 +452,10 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
 #pragma unroll
         for (int k = 0; k < N; ++k) v[k] = rd4(k, t);
         const int32_t g = gb + t;
-        if (g <= m.thr_tile)
+        // warp-uniform choice: the masked variant is exact for every lane,
+        // so a warp with any lane at or before its threshold tile runs it
+        // once instead of diverging into both variants
+        if (__any_sync(0xffffffffu, g <= m.thr_tile))
           quad_step<N, Hist, true>(m, ep, v, g, on_c);
         else
           quad_step<N, Hist, false>(m, ep, v, g, on_c);

@@ -97,6 +97,7 @@ Engine::~Engine() {
 // ---- deferred statistics -----------------------------------------------------
 
 void Engine::begin_op() {
+  ++stat_epoch_;
   ev_used_ = 0;
   timed_.clear();
   slot_counters_.clear();
@@ -114,18 +115,28 @@ cudaEvent_t Engine::next_event() {
 }
 
 int Engine::new_slot() {
+  ++stat_epoch_;
   if (log_used_ >= kLogSlots) throw Error(EPI_EUNSUPPORTED, "device statistics log exhausted");
   return log_used_++;
 }
 
-void Engine::flush_stats(epi_stats& stats) {
+void Engine::prefetch_stats() {
   const size_t nlog = static_cast<size_t>(log_used_);
-  char* h = static_cast<char*>(pin_small_.get(64 + nlog * sizeof(uint32_t)));
+  char* h = static_cast<char*>(pin_small_.get(64 + kLogSlots * sizeof(uint32_t)));
+  EPI_CUDA(cudaMemcpyAsync(h, d_acc_, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
+  if (nlog) EPI_CUDA(cudaMemcpyAsync(h + 64, d_log_, nlog * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+  prefetched_epoch_ = stat_epoch_;
+}
+
+void Engine::flush_stats(epi_stats& stats) {
+  const bool ready = prefetched_epoch_ == stat_epoch_;
+  if (!ready) prefetch_stats();
+  char* h = static_cast<char*>(pin_small_.get(64 + kLogSlots * sizeof(uint32_t)));
   auto* acc = reinterpret_cast<unsigned long long*>(h);
   auto* log = reinterpret_cast<uint32_t*>(h + 64);
-  EPI_CUDA(cudaMemcpyAsync(acc, d_acc_, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
-  if (nlog) EPI_CUDA(cudaMemcpyAsync(log, d_log_, nlog * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
-  EPI_CUDA(cudaStreamSynchronize(st_));
+  // the caller synchronised right after the prefetch when `ready`
+  if (!ready) EPI_CUDA(cudaStreamSynchronize(st_));
+  ++stat_epoch_;
   stats.patches += acc[0];
   stats.matched_pairs += acc[1];
   stats.pruned += acc[2];
@@ -279,6 +290,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   if (n == 0) return;
   const uint32_t N = ds.N;
   const uint32_t* n_dev = live_slot >= 0 ? slot_ptr(live_slot) : nullptr;
+  ++stat_epoch_;  // writes the statistics accumulators
   if (N == 1) {
     if (n_dev) throw Error(EPI_EUNSUPPORTED, "single-node sets need a host-known size");
     // every distinct firing time is a completion: popcount of the bitmap

@@ -129,6 +129,11 @@ class Engine {
   // resolves every recorded interval and device counter into `stats`.
   void begin_op();
   void flush_stats(epi_stats& stats);
+  // Enqueue the D2H of the statistics log right before a synchronisation the
+  // caller makes anyway; flush_stats then needs no extra round trip when
+  // nothing was launched in between.
+  void prefetch_stats();
+  uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
   cudaEvent_t next_event();
   int new_slot();  // a device u32 log slot, unique within the call
   uint32_t* slot_ptr(int s) { return d_log_ + s; }

@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 
 #include "common.cuh"
@@ -51,6 +53,23 @@ enum MineSlot : size_t {
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+// EPI_TRACE=1: host timestamps of the mining phases on stderr (diagnostics).
+struct HostTrace {
+  bool on = std::getenv("EPI_TRACE") != nullptr;
+  std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> pts;
+  void mark(const char* what) {
+    if (on) pts.emplace_back(what, std::chrono::steady_clock::now());
+  }
+  void dump() {
+    if (!on || pts.empty()) return;
+    for (size_t i = 1; i < pts.size(); ++i)
+      std::fprintf(stderr, "[epi trace] %-18s %8.1f us\n", pts[i].first,
+                   std::chrono::duration<double, std::micro>(pts[i].second - pts[i - 1].second).count());
+    pts.clear();
+  }
+};
+thread_local HostTrace g_trace;
 
 __global__ void gen_level2_kernel(const uint32_t* __restrict__ f1, uint32_t nf1,
                                   const uint32_t* __restrict__ awin, const uint32_t* __restrict__ ahi,
@@ -294,7 +313,9 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   map_small_.get(64);
   uint32_t* h_groups = static_cast<uint32_t*>(map_small_.p);
   dev_scan_total(flags, scan, n, new_slot(), h_groups);
+  g_trace.mark("p1 sort launched");
   EPI_CUDA(cudaStreamSynchronize(st_));
+  g_trace.mark("p1 groups synced");
   const uint32_t n_groups = *reinterpret_cast<volatile uint32_t*>(h_groups);
   stats.kernel_launches += 5;
   if (2ull * n_groups > n) {
@@ -407,6 +428,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
   m_hi_.clear();
   epi_stats totals{};
   begin_op();
+  g_trace.mark("mine start");
   const uint32_t A = stream_.alphabet;
 
   // Frequent set of the previous level, host side (types, packed windows).
@@ -453,6 +475,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
       nf = ftypes.size();
       record_level(A, 1, ftypes.data(), nullptr, fc.data(), nf,
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      g_trace.mark("level 1 done");
       if (nf == 0) break;
       continue;
     }
@@ -465,41 +488,77 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
       n = static_cast<uint64_t>(nf) * nf * cfg.n_alpha;
     } else {
       // Join index over the frequent set: stable sort by the prefix key
-      // (first L-2 nodes + their constraints), exact comparisons.
+      // (first L-2 nodes + their constraints); each left's bucket is the
+      // range of rights whose prefix key equals the left's suffix key. Keys
+      // are packed into 64 bits (type ids + constraint-alphabet indices)
+      // when they fit, else compared field by field.
       const uint32_t K = F - 1;
-      auto cmp_key = [&](uint32_t a, uint32_t fa, uint32_t b, uint32_t fb) -> int {
-        for (uint32_t k = 0; k < K; ++k) {
-          const uint32_t x = ftypes[static_cast<size_t>(a) * F + fa + k],
-                         y = ftypes[static_cast<size_t>(b) * F + fb + k];
-          if (x != y) return x < y ? -1 : 1;
-        }
-        for (uint32_t k = 0; k + 1 < K; ++k) {
-          const uint32_t x = fwin[static_cast<size_t>(a) * (F - 1) + fa + k],
-                         y = fwin[static_cast<size_t>(b) * (F - 1) + fb + k];
-          if (x != y) return x < y ? -1 : 1;
-        }
-        return 0;
-      };
+      uint32_t tbits = 1, wbits = 1;
+      while ((1ull << tbits) < A + 1ull) ++tbits;
+      while ((1ull << wbits) < cfg.n_alpha) ++wbits;
+      const bool packed = K * tbits + (K > 0 ? (K - 1) * wbits : 0) <= 64;
       pre.resize(nf);
-      std::iota(pre.begin(), pre.end(), 0u);
-      std::stable_sort(pre.begin(), pre.end(),
-                       [&](uint32_t a, uint32_t b) { return cmp_key(a, 0, b, 0) < 0; });
       lrange.resize(2 * nf);
       loff.assign(nf + 1, 0);
-      for (uint32_t l = 0; l < nf; ++l) {
-        auto lo = std::lower_bound(pre.begin(), pre.end(), l, [&](uint32_t r, uint32_t left) {
-          return cmp_key(r, 0, left, 1) < 0;
-        });
-        auto hi = std::upper_bound(lo, pre.end(), l, [&](uint32_t left, uint32_t r) {
-          return cmp_key(left, 1, r, 0) < 0;
-        });
-        const uint32_t b0 = static_cast<uint32_t>(lo - pre.begin()), b1 = static_cast<uint32_t>(hi - pre.begin());
-        lrange[2 * l] = b0;
-        lrange[2 * l + 1] = b1;
-        loff[l + 1] = loff[l] + (b1 - b0);
+      g_trace.mark("join alloc");
+      if (packed) {
+        auto widx = [&](uint32_t w) -> uint64_t {
+          for (uint64_t i = 0; i < cfg.n_alpha; ++i)
+            if (awin[i] == w) return i;
+          return 0;  // frequent windows always come from the alphabet
+        };
+        auto key = [&](size_t i, uint32_t first) {
+          uint64_t k = 0;
+          for (uint32_t j = 0; j < K; ++j) k = (k << tbits) | ftypes[i * F + first + j];
+          for (uint32_t j = 0; j + 1 < K; ++j) k = (k << wbits) | widx(fwin[i * (F - 1) + first + j]);
+          return k;
+        };
+        std::vector<std::pair<uint64_t, uint32_t>> pk(nf);
+        for (size_t i = 0; i < nf; ++i) pk[i] = {key(i, 0), static_cast<uint32_t>(i)};
+        std::sort(pk.begin(), pk.end());  // (key, index): ties keep frequent order
+        g_trace.mark("join sort");
+        for (size_t i = 0; i < nf; ++i) pre[i] = pk[i].second;
+        for (uint32_t l = 0; l < nf; ++l) {
+          const uint64_t k = key(l, 1);
+          auto lo = std::lower_bound(pk.begin(), pk.end(), std::make_pair(k, 0u));
+          auto hi = std::upper_bound(lo, pk.end(), std::make_pair(k, UINT32_MAX));
+          lrange[2 * l] = static_cast<uint32_t>(lo - pk.begin());
+          lrange[2 * l + 1] = static_cast<uint32_t>(hi - pk.begin());
+          loff[l + 1] = loff[l] + (hi - lo);
+        }
+      } else {
+        auto cmp_key = [&](uint32_t a, uint32_t fa, uint32_t b, uint32_t fb) -> int {
+          for (uint32_t k = 0; k < K; ++k) {
+            const uint32_t x = ftypes[static_cast<size_t>(a) * F + fa + k],
+                           y = ftypes[static_cast<size_t>(b) * F + fb + k];
+            if (x != y) return x < y ? -1 : 1;
+          }
+          for (uint32_t k = 0; k + 1 < K; ++k) {
+            const uint32_t x = fwin[static_cast<size_t>(a) * (F - 1) + fa + k],
+                           y = fwin[static_cast<size_t>(b) * (F - 1) + fb + k];
+            if (x != y) return x < y ? -1 : 1;
+          }
+          return 0;
+        };
+        std::iota(pre.begin(), pre.end(), 0u);
+        std::stable_sort(pre.begin(), pre.end(),
+                         [&](uint32_t a, uint32_t b) { return cmp_key(a, 0, b, 0) < 0; });
+        for (uint32_t l = 0; l < nf; ++l) {
+          auto lo = std::lower_bound(pre.begin(), pre.end(), l, [&](uint32_t r, uint32_t left) {
+            return cmp_key(r, 0, left, 1) < 0;
+          });
+          auto hi = std::upper_bound(lo, pre.end(), l, [&](uint32_t left, uint32_t r) {
+            return cmp_key(left, 1, r, 0) < 0;
+          });
+          const uint32_t b0 = static_cast<uint32_t>(lo - pre.begin()), b1 = static_cast<uint32_t>(hi - pre.begin());
+          lrange[2 * l] = b0;
+          lrange[2 * l + 1] = b1;
+          loff[l + 1] = loff[l] + (b1 - b0);
+        }
       }
       n = loff[nf];
     }
+    g_trace.mark("join index (host)");
     if (n == 0) break;
     if (n >= (1ull << 31)) throw Error(EPI_EUNSUPPORTED, "more than 2^31 candidates in one level");
 
@@ -566,7 +625,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     c.max_high = amax;
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
+    g_trace.mark("gen launched");
     if (cnt_c > 0) count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, d_counts + lo_c, totals);
+    g_trace.mark("count launched");
     if (sharded) {
       // every rank's s-wide slice -> the full count vector in candidate order
       uint64_t* d_all = scratch_.get<uint64_t>(kMGather, s * W);
@@ -592,7 +653,10 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(dm + o_t),
         reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c));
     EPI_CUDA(cudaGetLastError());
+    g_trace.mark("compact launched");
+    prefetch_stats();
     EPI_CUDA(cudaStreamSynchronize(st_));
+    g_trace.mark("level synced");
     totals.kernel_launches += 5;
     const uint32_t k = *reinterpret_cast<volatile uint32_t*>(h_k);
     const char* hm = static_cast<const char*>(map_out_.p);
@@ -608,9 +672,13 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     fwin.swap(nwin);
     F = L;
     nf = k;
+    g_trace.mark("level recorded");
     if (nf == 0) break;
   }
+  g_trace.mark("levels done");
   flush_stats(totals);
+  g_trace.mark("stats flushed");
+  g_trace.dump();
   out->n_levels = m_level_cands_.size();
   out->level_candidates = m_level_cands_.data();
   out->level_offsets = m_level_off_.data();
