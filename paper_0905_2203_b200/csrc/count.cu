@@ -15,6 +15,30 @@ EPI_EXTERN_W(5) EPI_EXTERN_W(6) EPI_EXTERN_W(7) EPI_EXTERN_W(8)
 EPI_EXTERN_W(9) EPI_EXTERN_W(10) EPI_EXTERN_W(11) EPI_EXTERN_W(12)
 EPI_EXTERN_W(13) EPI_EXTERN_W(14) EPI_EXTERN_W(15) EPI_EXTERN_W(16)
 #undef EPI_EXTERN_W
+#define EPI_EXTERN_L(W) \
+  extern template void impl::launch_machines_l<W>(int, const CountLaunch&, cudaStream_t);
+EPI_EXTERN_L(1) EPI_EXTERN_L(2) EPI_EXTERN_L(3) EPI_EXTERN_L(4)
+EPI_EXTERN_L(5) EPI_EXTERN_L(6) EPI_EXTERN_L(7) EPI_EXTERN_L(8)
+EPI_EXTERN_L(9) EPI_EXTERN_L(10) EPI_EXTERN_L(11) EPI_EXTERN_L(12)
+EPI_EXTERN_L(13) EPI_EXTERN_L(14) EPI_EXTERN_L(15) EPI_EXTERN_L(16)
+#undef EPI_EXTERN_L
+
+bool launch_machines_last(int n_nodes, int width, uint32_t w_last, CountLaunch& p, cudaStream_t st) {
+  if (n_nodes < 3 || n_nodes > 6 || width < 1 || width > 16 || w_last < 1 || w_last > 16) return false;
+  smear_shifts(w_last, p.last_sh);
+  switch (width) {
+#define EPI_CASE_L(W) \
+  case W:             \
+    impl::launch_machines_l<W>(n_nodes, p, st); \
+    return true;
+    EPI_CASE_L(1) EPI_CASE_L(2) EPI_CASE_L(3) EPI_CASE_L(4)
+    EPI_CASE_L(5) EPI_CASE_L(6) EPI_CASE_L(7) EPI_CASE_L(8)
+    EPI_CASE_L(9) EPI_CASE_L(10) EPI_CASE_L(11) EPI_CASE_L(12)
+    EPI_CASE_L(13) EPI_CASE_L(14) EPI_CASE_L(15) EPI_CASE_L(16)
+#undef EPI_CASE_L
+  }
+  return false;
+}
 
 int32_t stages_for(uint32_t blk_words) {
   const uint32_t bytes = blk_words * 4u;

@@ -35,7 +35,18 @@ struct CountLaunch {
   uint64_t* counts;          // [n_eps] walk output (map output when P == 1)
   unsigned long long* patches;  // walk statistics counter
   int* occ_query;            // host: non-null -> launch_machines* reports CTAs/SM, no launch
+  uint32_t last_sh[4];       // launch_machines_last: doubling-smear shifts of the last window
 };
+
+// Doubling-smear shift amounts covering a window of width w (1..16).
+inline void smear_shifts(uint32_t w, uint32_t (&sh)[4]) {
+  uint32_t cover = 1;
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t s = cover < w ? (cover < w - cover ? cover : w - cover) : 0u;
+    sh[i] = s;
+    cover += s;
+  }
+}
 
 // Shared-memory ring depth for a bitmap block of blk_words words.
 int32_t stages_for(uint32_t blk_words);
@@ -43,6 +54,11 @@ int32_t stages_for(uint32_t blk_words);
 // high <= 32. Together they select a specialised map kernel when available.
 void launch_machines(int n_nodes, int width, bool hi32, const CountLaunch& p, cudaStream_t st);
 void launch_walk(int n_nodes, const CountLaunch& p, cudaStream_t st);
+// Pass-1 shape: every window but the last has width `width` (1..16), the last
+// one a launch-uniform width w_last <= 16 (p.last_sh), every high <= 32,
+// n_nodes 3..6. Returns false (nothing launched) when the shape has no
+// specialised kernel.
+bool launch_machines_last(int n_nodes, int width, uint32_t w_last, CountLaunch& p, cudaStream_t st);
 // high > 63 (up to kMaxHighWide): local-memory history ring.
 void launch_machines_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);

@@ -171,8 +171,27 @@ __device__ __forceinline__ uint32_t window_any(uint32_t c, uint32_t h1, uint32_t
 // high <= 63: the entry bitmaps of the previous tiles, in registers (two
 // words; one when every high <= 32). W > 0: every window of the launch has
 // width high - low == W (compile-time unrolled smear); W == 0: runtime.
-template <int N, int W = 0, bool kHi32 = false>
+// Window test of the last constraint when it alone has a different,
+// launch-uniform width (pass 1 relaxes only the last constraint to the
+// constraint alphabet's hull, high <= 32): a doubling smear whose four shift
+// amounts are kernel parameters (constant bank), so the other positions keep
+// the compile-time width W.
+__device__ __forceinline__ uint32_t window_last(uint32_t c, uint32_t h1, uint32_t hi,
+                                                const CountLaunch& p) {
+  const uint32_t s = 32u - hi;
+  uint32_t rl = __funnelshift_r(h1, c, s), rh = c >> s;
+  rl |= __funnelshift_r(rl, rh, p.last_sh[0]);
+  rh |= rh >> p.last_sh[0];
+  rl |= __funnelshift_r(rl, rh, p.last_sh[1]);
+  rh |= rh >> p.last_sh[1];
+  rl |= __funnelshift_r(rl, rh, p.last_sh[2]);
+  rh |= rh >> p.last_sh[2];
+  return rl | __funnelshift_r(rl, rh, p.last_sh[3]);
+}
+
+template <int N, int W = 0, bool kHi32 = false, bool kLast = false>
 struct NarrowHist {
+  static_assert(!kLast || (kHi32 && W > 0), "last-position smear needs high <= 32 and a uniform W");
   static constexpr bool kQuad = true;  // four tiles per 16-byte load, unrolled
   static constexpr int M = N > 1 ? N - 1 : 1;
   static constexpr int M2 = kHi32 ? 1 : M;
@@ -196,11 +215,18 @@ struct NarrowHist {
              window_any<0, kHi32>(c, h1, h2, lo1 + 32u, hi);
     }
   }
-  __device__ __forceinline__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi,
-                                             int32_t) const {
+  __device__ __forceinline__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi, int32_t,
+                                             const CountLaunch& p) const {
+    if constexpr (kLast) {
+      if (k == N - 2) return window_last(c, h1[k], hi, p);
+    }
     return dil(c, h1[k], kHi32 ? 0u : h2[kHi32 ? 0 : k], lo1, hi);
   }
-  __device__ __forceinline__ static uint32_t dilate_fresh(uint32_t c, uint32_t lo1, uint32_t hi) {
+  __device__ __forceinline__ static uint32_t dilate_fresh(int k, uint32_t c, uint32_t lo1, uint32_t hi,
+                                                          const CountLaunch& p) {
+    if constexpr (kLast) {
+      if (k == N - 2) return window_last(c, 0u, hi, p);
+    }
     return dil(c, 0u, 0u, lo1, hi);
   }
   __device__ __forceinline__ void push(const uint32_t* C, int32_t) {
@@ -247,7 +273,8 @@ struct WideHist {
     const int w = x >> 5, s = x & 31;
     return __funnelshift_r(word(k, w, c, g), word(k, w + 1, c, g), s);
   }
-  __device__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi, int32_t g) const {
+  __device__ uint32_t dilate(int k, uint32_t c, uint32_t lo1, uint32_t hi, int32_t g,
+                             const CountLaunch&) const {
     const int A = static_cast<int>(lo1), B = static_cast<int>(hi);
     const int P0 = 32 * hw - B, P1 = 32 * hw - A;
     const int w = B - A + 1;  // window width (high - low)
@@ -285,7 +312,8 @@ struct WideHist {
     sr |= sr << 16;
     return (any ? ~0u : 0u) | sl | sr;
   }
-  __device__ __forceinline__ static uint32_t dilate_fresh(uint32_t c, uint32_t lo1, uint32_t hi) {
+  __device__ __forceinline__ static uint32_t dilate_fresh(int, uint32_t c, uint32_t lo1, uint32_t hi,
+                                                          const CountLaunch&) {
     uint32_t d = 0;
     const uint32_t e1 = hi < 31u ? hi : 31u;
     for (uint32_t a = lo1; a <= e1; ++a) d |= c << a;
@@ -321,7 +349,8 @@ struct Machine {
 // kMask: the tile may lie at or before the position-0 threshold tile.
 template <int N, class Hist, bool kMask, class OnC>
 __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>& ep,
-                                          const uint32_t (&occ)[N], int32_t g, OnC&& on_c) {
+                                          const uint32_t (&occ)[N], int32_t g, const CountLaunch& p,
+                                          OnC&& on_c) {
   uint32_t C[N];
   C[0] = occ[0];
   if constexpr (kMask) {
@@ -329,7 +358,7 @@ __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>
   }
 #pragma unroll
   for (int k = 1; k < N; ++k)
-    C[k] = occ[k] & m.hist.dilate(k - 1, C[k - 1], ep.lo1[k - 1], ep.hi[k - 1], g);
+    C[k] = occ[k] & m.hist.dilate(k - 1, C[k - 1], ep.lo1[k - 1], ep.hi[k - 1], g, p);
   if (C[N - 1]) {
     uint32_t last = C[N - 1];
     do {
@@ -341,7 +370,8 @@ __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>
       m.thr_mask = msk;
       C[0] = occ[0] & msk;
 #pragma unroll
-      for (int k = 1; k < N; ++k) C[k] = occ[k] & Hist::dilate_fresh(C[k - 1], ep.lo1[k - 1], ep.hi[k - 1]);
+      for (int k = 1; k < N; ++k)
+        C[k] = occ[k] & Hist::dilate_fresh(k - 1, C[k - 1], ep.lo1[k - 1], ep.hi[k - 1], p);
       last = C[N - 1];
     } while (last);
     m.hist.on_clear(g);  // the clear also empties older history
@@ -356,20 +386,21 @@ __device__ __forceinline__ bool tile_step(Machine<N, Hist>& m, const EpParams<N>
 // so the warp replays the quad anyway.)
 template <int N, class Hist, bool kMask, class OnC>
 __device__ __forceinline__ void quad_step(Machine<N, Hist>& m, const EpParams<N>& ep,
-                                          const uint4 (&v)[N], int32_t g, OnC&& on_c) {
+                                          const uint4 (&v)[N], int32_t g, const CountLaunch& p,
+                                          OnC&& on_c) {
   uint32_t o[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) o[k] = v[k].x;
-  tile_step<N, Hist, kMask>(m, ep, o, g, on_c);
+  tile_step<N, Hist, kMask>(m, ep, o, g, p, on_c);
 #pragma unroll
   for (int k = 0; k < N; ++k) o[k] = v[k].y;
-  tile_step<N, Hist, kMask>(m, ep, o, g + 1, on_c);
+  tile_step<N, Hist, kMask>(m, ep, o, g + 1, p, on_c);
 #pragma unroll
   for (int k = 0; k < N; ++k) o[k] = v[k].z;
-  tile_step<N, Hist, kMask>(m, ep, o, g + 2, on_c);
+  tile_step<N, Hist, kMask>(m, ep, o, g + 2, p, on_c);
 #pragma unroll
   for (int k = 0; k < N; ++k) o[k] = v[k].w;
-  tile_step<N, Hist, kMask>(m, ep, o, g + 3, on_c);
+  tile_step<N, Hist, kMask>(m, ep, o, g + 3, p, on_c);
 }
 
 // Map step: FRESH machine of (episode, segment). The CTA walks the bitmap
@@ -456,16 +487,16 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
         // so a warp with any lane at or before its threshold tile runs it
         // once instead of diverging into both variants
         if (__any_sync(0xffffffffu, g <= m.thr_tile))
-          quad_step<N, Hist, true>(m, ep, v, g, on_c);
+          quad_step<N, Hist, true>(m, ep, v, g, p, on_c);
         else
-          quad_step<N, Hist, false>(m, ep, v, g, on_c);
+          quad_step<N, Hist, false>(m, ep, v, g, p, on_c);
       }
     } else {
       for (int32_t t = t0; t < t1; ++t) {
         uint32_t o[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) o[k] = rd1(k, t);
-        tile_step<N, Hist, true>(m, ep, o, gb + t, on_c);
+        tile_step<N, Hist, true>(m, ep, o, gb + t, p, on_c);
       }
     }
   };
@@ -609,7 +640,7 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
         uint32_t occ[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) occ[k] = __ldg(p.occ + occ_index(g, ep.type[k], p.blk_words));
-        if (tile_step<N, Hist, true>(m, ep, occ, g, on_c)) break;
+        if (tile_step<N, Hist, true>(m, ep, occ, g, p, on_c)) break;
       }
       if (!synced) {
         cnt = rc;
@@ -703,6 +734,19 @@ struct NarrowW {
 template <int W>
 void launch_machines_w(int n, const CountLaunch& p, cudaStream_t st) {
   Dispatch<NarrowW<W, true>::template H, 2, 3, 4, 5, 6, 7, 8>::machines(n, p, st);
+}
+
+template <int W>
+struct NarrowL {
+  template <int N>
+  using H = NarrowHist<N, W, true, true>;
+};
+
+// Pass-1 map kernels: width W at every position but the last, whose window
+// (launch-uniform width <= 16, high <= 32) uses window_last (count_l*.cu).
+template <int W>
+void launch_machines_l(int n, const CountLaunch& p, cudaStream_t st) {
+  Dispatch<NarrowL<W>::template H, 3, 4, 5, 6>::machines(n, p, st);
 }
 }  // namespace impl
 }  // namespace epi

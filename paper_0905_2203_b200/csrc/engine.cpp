@@ -242,7 +242,9 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
   ds.N = N;
   ds.n = n;
   const uint32_t A = stream_.alphabet;
-  int64_t width = -1;  // launch-uniform window width high-low, 0 if mixed
+  // launch-uniform window width high-low of the constraints before the last
+  // (width) and of the last one (width_last); -1 unset, 0 mixed
+  int64_t width = -1, width_last = -1;
   for (size_t e = 0; e < n; ++e) {
     for (uint32_t k = 0; k < N; ++k) {
       uint32_t t = set.types[e * N + k];
@@ -256,15 +258,21 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
       h_win[e * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
       sig += static_cast<uint32_t>(hi);
       ds.max_high = std::max(ds.max_high, hi);
-      if (width == -1)
-        width = hi - lo;
-      else if (width != hi - lo)
-        width = 0;
+      int64_t& w = k + 1 < M ? width : width_last;
+      if (w == -1)
+        w = hi - lo;
+      else if (w != hi - lo)
+        w = 0;
     }
     h_sigma[e] = sig;
     ds.max_sigma = std::max(ds.max_sigma, sig);
   }
-  ds.width = width > 0 ? static_cast<int>(width) : 0;
+  if (width == -1 || width == width_last) {
+    ds.width = width_last > 0 ? static_cast<int>(width_last) : 0;
+  } else if (width > 0 && width_last > 0) {
+    ds.width = static_cast<int>(width);  // the last constraint alone differs
+    ds.last_w = static_cast<uint32_t>(width_last);
+  }
   char* d_params = scratch_.get<char>(kSlotParams, total);
   EPI_CUDA(cudaMemcpyAsync(d_params, host, total, cudaMemcpyHostToDevice, st_));
   stats.h2d_bytes += total;
@@ -327,8 +335,11 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   auto launch_map = [&]() {
     if (wide)
       launch_machines_wide(static_cast<int>(N), p, st_);
+    else if (ds.last_w && ds.max_high <= 32 &&
+             launch_machines_last(static_cast<int>(N), ds.width, ds.last_w, p, st_))
+      return;
     else
-      launch_machines(static_cast<int>(N), ds.width, ds.max_high <= 32, p, st_);
+      launch_machines(static_cast<int>(N), ds.last_w ? 0 : ds.width, ds.max_high <= 32, p, st_);
   };
 
   // MapConcatenate plan. Segments must each span sum(high) (the window of a
@@ -349,7 +360,8 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const uint64_t shape = (static_cast<uint64_t>(N) << 48) ^ (static_cast<uint64_t>(ds.width) << 40) ^
                          (static_cast<uint64_t>(ds.max_high <= 32) << 39) ^
                          (static_cast<uint64_t>(wide) << 38) ^
-                         (static_cast<uint64_t>(p.stages) << 32) ^ p.blk_words;
+                         (static_cast<uint64_t>(p.stages) << 32) ^ p.blk_words ^
+                         (static_cast<uint64_t>(ds.last_w) << 56);
   int bps = 0;
   for (const auto& kv : occ_cache_)
     if (kv.first == shape) bps = kv.second;

@@ -38,6 +38,8 @@ struct DevSet {
   uint32_t max_sigma = 0;
   int64_t max_high = 0;
   int width = 0;                    // launch-uniform high-low, 0 if mixed
+  uint32_t last_w = 0;              // != 0: the last constraint alone has this
+                                    // launch-uniform width; `width` covers the others
 };
 
 // Host memory the device writes directly (zero-copy): small, sparse outputs
@@ -118,7 +120,8 @@ class Engine {
                     int live_slot = -1);
   // uniform_win != 0: pass-1 relaxation uses that window at every position.
   void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
-                             uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats);
+                             uint32_t uniform_win, const uint32_t* alpha, uint32_t n_alpha,
+                             uint64_t* d_counts, epi_stats& stats);
   // Exclusive scan of n u32 flags; the total goes to device log slot `slot`
   // (and to *host_total, zero-copy, when given). No host synchronisation.
   void dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, int slot,

@@ -115,12 +115,29 @@ __global__ void gen_join_kernel(uint32_t L, const uint32_t* __restrict__ ftypes,
   }
 }
 
-__global__ void pack_keys_kernel(const uint32_t* __restrict__ types, uint32_t L, uint32_t bits,
+// Constraint alphabet by value (window -> index for the grouping keys).
+struct AlphaWin {
+  uint32_t w[16];
+  uint32_t n;
+};
+
+// Grouping key of pass 1: the type sequence, plus (with wbits > 0) the
+// alphabet indices of every constraint but the last.
+__global__ void pack_keys_kernel(const uint32_t* __restrict__ types, const uint32_t* __restrict__ win,
+                                 uint32_t L, uint32_t bits, uint32_t wbits, const AlphaWin aw,
                                  uint64_t n, uint64_t* keys, uint32_t* idx) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint64_t k = 0;
   for (uint32_t j = 0; j < L; ++j) k = (k << bits) | types[i * L + j];
+  if (wbits)
+    for (uint32_t j = 0; j + 2 < L; ++j) {
+      const uint32_t w = win[i * (L - 1) + j];
+      uint32_t x = 0;
+      for (uint32_t a = 0; a < aw.n; ++a)
+        if (aw.w[a] == w) x = a;
+      k = (k << wbits) | x;
+    }
   keys[i] = k;
   idx[i] = static_cast<uint32_t>(i);
 }
@@ -140,15 +157,17 @@ __global__ void group_starts_kernel(const uint32_t* __restrict__ flags,
   if (flags[j]) gstart[scan[j]] = static_cast<uint32_t>(j);
 }
 
-// One thread per group: the relaxed episode of the group. With
-// uniform_win != 0 every constraint becomes that window (the hull of the
-// whole constraint alphabet: contains every member's window, so still a sound
-// bound, and launch-uniform, so pass 1 runs on the width-specialised
-// kernels); otherwise the per-position hull of the members' windows.
+// One thread per group: the relaxed episode of the group. With last_only the
+// group shares every constraint but the last (they are part of its key) and
+// only the last one is relaxed; with uniform_win != 0 a relaxed constraint
+// becomes that window (the hull of the whole constraint alphabet: contains
+// every member's window, so still a sound bound, and launch-uniform, so pass
+// 1 runs on width-specialised kernels); otherwise the per-position hull of
+// the members' windows.
 __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* __restrict__ win,
                             uint32_t L, const uint32_t* __restrict__ idx_sorted,
                             const uint32_t* __restrict__ gstart, uint32_t n_groups, uint64_t n,
-                            uint32_t uniform_win, uint32_t* rtypes, uint32_t* rwin,
+                            uint32_t uniform_win, bool last_only, uint32_t* rtypes, uint32_t* rwin,
                             uint32_t* rsigma, uint32_t* gsize) {
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_groups) return;
@@ -160,7 +179,12 @@ __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* 
   uint32_t sig = 0;
   for (uint32_t k = 0; k < M; ++k) {
     uint32_t lo1 = 0xffffu, hi = 0;
-    if (uniform_win) {
+    if (last_only && k + 1 < M) {
+      // grouped by these windows too: every member has the first's
+      const uint32_t w = win[static_cast<size_t>(first) * M + k];
+      lo1 = w & 0xffffu;
+      hi = w >> 16;
+    } else if (uniform_win) {
       lo1 = uniform_win & 0xffffu;
       hi = uniform_win >> 16;
     } else {
@@ -272,7 +296,8 @@ void Engine::dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, i
 // synchronisation (the group count decides whether pass 1 pays); survivors
 // are sized on the device.
 void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
-                                   uint32_t uniform_win, uint64_t* d_counts, epi_stats& stats) {
+                                   uint32_t uniform_win, const uint32_t* alpha, uint32_t n_alpha,
+                                   uint64_t* d_counts, epi_stats& stats) {
   const uint64_t n = c.n;
   const uint32_t L = c.N;
   stats.episodes += n;
@@ -290,20 +315,36 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
     return;
   }
   const uint32_t M = L - 1;
+  // Relaxation: only the last constraint, to the alphabet hull, grouping by
+  // types + the other constraints (tight bounds: on cfg2 level 3 it leaves
+  // 51 of 142,228 candidates for pass 2, against 126,512 when every
+  // constraint is relaxed); the types-only grouping with every constraint
+  // relaxed when the key does not fit 64 bits or the alphabet is large.
+  AlphaWin aw{};
+  uint32_t wbits = 0;
+  if (L >= 3 && uniform_win && n_alpha <= 16) {
+    wbits = 1;
+    while ((1u << wbits) < n_alpha) ++wbits;
+    if (bits * L + wbits * (L - 2) > 64) wbits = 0;
+    for (uint32_t a = 0; a < n_alpha; ++a) aw.w[a] = alpha[a];
+    aw.n = n_alpha;
+  }
+  const bool last_only = wbits > 0;
+  const uint32_t key_bits = bits * L + wbits * (L >= 2 ? L - 2 : 0);
   uint64_t* keys = scratch_.get<uint64_t>(kMKeys, n);
   uint64_t* keys_alt = scratch_.get<uint64_t>(kMKeysAlt, n);
   uint32_t* idx = scratch_.get<uint32_t>(kMIdx, n);
   uint32_t* idx_alt = scratch_.get<uint32_t>(kMIdxAlt, n);
-  pack_keys_kernel<<<blocks_for(n), 256, 0, st_>>>(c.types, L, bits, n, keys, idx);
+  pack_keys_kernel<<<blocks_for(n), 256, 0, st_>>>(c.types, c.win, L, bits, wbits, aw, n, keys, idx);
   EPI_CUDA(cudaGetLastError());
   cub::DoubleBuffer<uint64_t> kb(keys, keys_alt);
   cub::DoubleBuffer<uint32_t> vb(idx, idx_alt);
   size_t tmp = 0;
   EPI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(n), 0,
-                                           static_cast<int>(bits * L), st_));
+                                           static_cast<int>(key_bits), st_));
   void* d_tmp = scratch_.get<char>(kMCub, tmp + 16);
   EPI_CUDA(cub::DeviceRadixSort::SortPairs(d_tmp, tmp, kb, vb, static_cast<int>(n), 0,
-                                           static_cast<int>(bits * L), st_));
+                                           static_cast<int>(key_bits), st_));
   const uint64_t* skeys = kb.Current();
   const uint32_t* sidx = vb.Current();
   uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
@@ -339,7 +380,8 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   uint32_t* gsize = reinterpret_cast<uint32_t*>(gbuf + g_size);
   group_starts_kernel<<<blocks_for(n), 256, 0, st_>>>(flags, scan, n, gstart);
   hull_kernel<<<blocks_for(n_groups), 256, 0, st_>>>(c.types, c.win, L, sidx, gstart, n_groups, n,
-                                                     uniform_win, rtypes, rwin, rsigma, gsize);
+                                                     uniform_win, last_only, rtypes, rwin, rsigma,
+                                                     gsize);
   EPI_CUDA(cudaGetLastError());
   stats.kernel_launches += 2;
   DevSet rel = c;
@@ -348,7 +390,13 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   rel.win = rwin;
   rel.sigma = rsigma;
   // per-group hull widths differ in general; the alphabet hull is uniform
-  rel.width = uniform_win ? static_cast<int>((uniform_win >> 16) - (uniform_win & 0xffffu) + 1) : 0;
+  const int hull_w = uniform_win ? static_cast<int>((uniform_win >> 16) - (uniform_win & 0xffffu) + 1) : 0;
+  if (last_only) {
+    rel.width = c.width;  // the kept constraints
+    rel.last_w = static_cast<uint32_t>(hull_w);
+  } else {
+    rel.width = hull_w;
+  }
   if (uniform_win) rel.max_sigma = (uniform_win >> 16) * (L - 1);
   uint64_t* bound = scratch_.get<uint64_t>(kMGroupCnt, n_groups);
   stats.pass1_groups += n_groups;
@@ -626,7 +674,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
     g_trace.mark("gen launched");
-    if (cnt_c > 0) count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, d_counts + lo_c, totals);
+    if (cnt_c > 0)
+      count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, awin.data(),
+                            static_cast<uint32_t>(cfg.n_alpha), d_counts + lo_c, totals);
     g_trace.mark("count launched");
     if (sharded) {
       // every rank's s-wide slice -> the full count vector in candidate order

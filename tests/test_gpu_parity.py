@@ -323,3 +323,35 @@ def test_million_candidates(ctx):
                                             (int(lo[2 * i + 1]), int(lo[2 * i + 1]) + 5)]) for i in pick])
     want = oracle.count_batch(types, times, sub.offsets, sub.types, sub.low, sub.high, threads=16)
     np.testing.assert_array_equal(got[pick], want)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_uniform_head_last_width_vs_port(ctx, seed, segments_env):
+    """Batches whose constraints before the last share one width W and whose
+    last constraints share another width WL (the shape of the miner's pass-1
+    hull episodes) take the launch_machines_last kernels; every high <= 32."""
+    rng = np.random.default_rng(7000 + seed)
+    for it in range(24):
+        segments_env([None, 4, 9][it % 3])
+        n_types = int(rng.integers(3, 9))
+        n_ev = 3000
+        times = np.cumsum(rng.integers(0, [3, 12, 60][it % 3] + 1, n_ev)).astype(np.int64)
+        types = rng.integers(0, n_types, n_ev).astype(np.uint32)
+        W = int(rng.integers(1, 17))
+        WL = int(rng.integers(1, 17))
+        eps = []
+        for _ in range(int(rng.integers(40, 300))):
+            N = int(rng.integers(3, 7))
+            cons = []
+            for k in range(N - 1):
+                w = W if k + 1 < N - 1 else WL
+                lo = int(rng.integers(0, 32 - w + 1))
+                cons.append((lo, lo + w))
+            eps.append(([int(x) for x in rng.integers(0, n_types, N)], cons))
+        # one length per batch keeps the launch on a single specialised kernel
+        N0 = len(eps[0][0])
+        eps = [e for e in eps if len(e[0]) == N0]
+        got = count_one(ctx, types, times, n_types, eps)
+        csr = csr_of(eps)
+        want = oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=4)
+        np.testing.assert_array_equal(got, want, err_msg=f"seed {seed} it {it} W {W} WL {WL}")
