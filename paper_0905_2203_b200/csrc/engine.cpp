@@ -450,15 +450,18 @@ void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
     count_exact(set, counts, stats, &stats.pass2_ms);
     return;
   }
-  // Pass 1: one relaxed episode per distinct type sequence, each constraint
-  // widened to the hull (min low, max high] over the sequence's variants.
-  // Every variant's occurrences are occurrences of the hull episode, and a
+  // Pass 1: one relaxed episode per group of candidates that agree on the
+  // types and on every constraint but the last; the last constraint is
+  // widened to the hull (min low, max high] of the group's last constraints.
+  // Every member's occurrences are occurrences of the relaxed episode, and a
   // maximum non-overlapped set cannot shrink when occurrences are added, so
-  // count(hull) >= count(variant): a sound upper bound. Singleton groups are
-  // exact already.
+  // count(relaxed) >= count(member): a sound upper bound. Relaxing only the
+  // last constraint keeps the bound tight (the device miner does the same,
+  // mine_dev.cu). Singleton groups are exact already.
   const uint32_t N = set.N, M = N - 1;
-  // Open-addressing table keyed by the type-sequence hash; slots hold group
-  // ids, collisions are resolved by comparing the stored type sequence.
+  const uint32_t KM = M - 1;  // constraints in the key
+  // Open-addressing table keyed by a hash of the key; slots hold group ids,
+  // collisions are resolved by comparing the stored key.
   size_t cap = 1;
   while (cap < 2 * n) cap <<= 1;
   std::vector<uint32_t> table(cap, UINT32_MAX);
@@ -467,15 +470,22 @@ void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
   relaxed.N = N;
   relaxed.types.reserve(n * N / 4 + N);
   std::vector<uint32_t> gsize;
-  std::vector<uint32_t> grep;
+  auto same_key = [&](uint32_t g, size_t i) {
+    if (std::memcmp(&relaxed.types[static_cast<size_t>(g) * N], &set.types[i * N], N * 4) != 0) return false;
+    for (uint32_t k = 0; k < KM; ++k)
+      if (relaxed.lo[static_cast<size_t>(g) * M + k] != set.lo[i * M + k] ||
+          relaxed.hi[static_cast<size_t>(g) * M + k] != set.hi[i * M + k])
+        return false;
+    return true;
+  };
   for (size_t i = 0; i < n; ++i) {
     const uint32_t* t = &set.types[i * N];
-    uint64_t h = hash_span(t, N, nullptr, nullptr, 0);
+    uint64_t h = hash_span(t, N, &set.lo[i * M], &set.hi[i * M], KM);
     size_t slot = static_cast<size_t>(h ^ (h >> 29)) & (cap - 1);
     uint32_t g = UINT32_MAX;
     while (table[slot] != UINT32_MAX) {
       const uint32_t gi = table[slot];
-      if (std::memcmp(&relaxed.types[static_cast<size_t>(gi) * N], t, N * 4) == 0) {
+      if (same_key(gi, i)) {
         g = gi;
         break;
       }
@@ -488,15 +498,12 @@ void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
       relaxed.lo.insert(relaxed.lo.end(), &set.lo[i * M], &set.lo[i * M] + M);
       relaxed.hi.insert(relaxed.hi.end(), &set.hi[i * M], &set.hi[i * M] + M);
       gsize.push_back(1);
-      grep.push_back(static_cast<uint32_t>(i));
     } else {
       ++gsize[g];
-      for (uint32_t k = 0; k < M; ++k) {
-        int64_t& lo = relaxed.lo[static_cast<size_t>(g) * M + k];
-        int64_t& hi = relaxed.hi[static_cast<size_t>(g) * M + k];
-        lo = std::min(lo, set.lo[i * M + k]);
-        hi = std::max(hi, set.hi[i * M + k]);
-      }
+      int64_t& lo = relaxed.lo[static_cast<size_t>(g) * M + KM];
+      int64_t& hi = relaxed.hi[static_cast<size_t>(g) * M + KM];
+      lo = std::min(lo, set.lo[i * M + KM]);
+      hi = std::max(hi, set.hi[i * M + KM]);
     }
     group[i] = g;
   }

@@ -122,6 +122,21 @@ class Engine {
   void count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t mode,
                              uint32_t uniform_win, const uint32_t* alpha, uint32_t n_alpha,
                              uint64_t* d_counts, epi_stats& stats);
+  // Left-grouped candidates of a mining level (the popcount pass 1): left l
+  // (a frequent (L-1)-episode) owns candidates [off[l], off[l+1]) (or
+  // [l*stride, (l+1)*stride) when off is null); the set counted here is the
+  // slice starting at candidate slice_lo.
+  struct PopLefts {
+    uint64_t nf = 0;
+    const uint32_t* types = nullptr;  // [nf * (L-1)]
+    const uint32_t* win = nullptr;    // [nf * (L-2)]
+    const uint64_t* off = nullptr;
+    uint64_t stride = 0;
+    uint64_t slice_lo = 0;
+  };
+  void count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t threshold,
+                             const uint32_t* alpha, uint32_t n_alpha, uint64_t* d_counts,
+                             epi_stats& stats);
   // Exclusive scan of n u32 flags; the total goes to device log slot `slot`
   // (and to *host_total, zero-copy, when given). No host synchronisation.
   void dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, int slot,

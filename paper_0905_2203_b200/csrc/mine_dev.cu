@@ -24,6 +24,7 @@
 #include <numeric>
 
 #include "common.cuh"
+#include "count_impl.cuh"
 #include "engine.h"
 
 namespace epi {
@@ -50,6 +51,7 @@ enum MineSlot : size_t {
   kMSurv,      // survivor params
   kMSurvCnt,
   kMGather,    // all-gathered level counts (sharded mining)
+  kMBound,     // pass-1 popcount bounds
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -201,6 +203,204 @@ __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* 
   gsize[g] = j1 - j0;
 }
 
+// ---- pass 1, popcount bound ------------------------------------------------
+// U(e)[t] = 1 iff some chain of e (no clears, no pe) ends at time t:
+//   U(tau) = occ(tau),  U(e ++ w ++ tau) = occ(tau) & dil_w(U(e)).
+// Every completion the exact counter makes is the end of a chain at a
+// distinct time, so count(c) <= popcount(U(c)): a sound bound. For a
+// candidate c = left ++ w ++ tau, popcount(occ(tau) & dil_w(U(left))) is an
+// AND-POPC of two bit rows; the dil_w(U(left)) rows are shared by all of the
+// left's candidates (one block per left), and there is no automaton state,
+// clear or divergence. On cfg2 level 3 it leaves 11 of 142,228 candidates.
+// Needs every high <= 32 (one history word).
+// Pass 1 only pays when a level is large: smaller levels (< kMinPass1
+// candidates) are cheaper to count exactly than to bound, prune and gather.
+// (EPI_PASS1_MIN overrides it: tests run pass 1 on small random levels.)
+constexpr uint64_t kMinPass1Default = 16384;
+uint64_t min_pass1() {
+  const char* s = std::getenv("EPI_PASS1_MIN");
+  return s ? static_cast<uint64_t>(std::strtoull(s, nullptr, 10)) : kMinPass1Default;
+}
+constexpr int kBoundThreads = 256;
+constexpr int kBoundMaxL = 16;
+
+struct BoundLaunch {
+  const uint32_t* occ;
+  uint32_t blk_words;
+  int32_t n_tiles;
+  uint32_t L;                      // candidate length (lefts have L-1 nodes)
+  const uint32_t* ltypes;          // [nf * (L-1)]
+  const uint32_t* lwin;            // [nf * (L-2)]
+  const uint64_t* loff;            // [nf + 1] candidates of left l (or null: l * stride)
+  uint64_t stride;
+  const uint32_t* ctypes;          // [n * L]
+  const uint32_t* cwin;            // [n * (L-1)]
+  AlphaWin aw;
+  int32_t span;                    // tiles per blockIdx.y split (multiple of kBoundThreads)
+  uint32_t uniform_w;              // every alphabet window has width high-low == uniform_w (0: mixed)
+  uint32_t sm[5];                  // doubling-smear shifts covering uniform_w
+  uint32_t n_sm;                   // steps used
+  uint64_t slice_lo, slice_hi;     // candidates counted here (episode shard)
+  unsigned long long* bound;       // [slice_hi - slice_lo], zeroed
+};
+
+__device__ __forceinline__ uint32_t dil_rt(uint32_t w, uint32_t h, uint32_t c) {
+  return impl::window_any<0, true>(c, h, 0u, w & 0xffffu, w >> 16);
+}
+
+// Equal-width alphabets (every window high - low == W): S = OR_{b<W} X >> b
+// over X = (c : h) once (64-bit doubling smear, shifts p.sm[]), then each
+// window [lo+1, hi] is one funnel shift of S by 32 - hi.
+struct Smear64 {
+  uint32_t lo, hi;
+};
+__device__ __forceinline__ Smear64 smear64(uint32_t h, uint32_t c, const uint32_t (&sh)[5], uint32_t steps) {
+  uint32_t rl = h, rh = c;
+  for (uint32_t i = 0; i < steps; ++i) {
+    rl |= __funnelshift_r(rl, rh, sh[i]);
+    rh |= rh >> sh[i];
+  }
+  return {rl, rh};
+}
+__device__ __forceinline__ uint32_t window_of(const Smear64& s, uint32_t w) {
+  return __funnelshift_r(s.lo, s.hi, 32u - (w >> 16));
+}
+
+// One block per (left, time split). Per chunk of 256 tiles: phase A, one
+// thread per tile, rebuilds U(left) from the type bitmaps (no state carried
+// across tiles, so any split is exact) and writes dil_w(U(left)) for every
+// alphabet window to shared memory; phase B, lane = tile (coalesced bitmap
+// rows), each warp accumulates AND-POPC sums for up to kBoundPerWarp of the
+// left's candidates in registers; one warp reduction per candidate at the end.
+constexpr int kBoundPerWarp = 16;
+constexpr int kBoundRound = kBoundPerWarp * (kBoundThreads / 32);
+
+// kF > 0: left length known at compile time (mining levels 2..7: U chain in
+// registers, loops unrolled); kF == 0: runtime length up to kBoundMaxL - 1.
+template <int kF>
+__global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch p) {
+  __shared__ uint32_t D[16][kBoundThreads];
+  __shared__ uint32_t s_tau[kBoundRound], s_widx[kBoundRound];
+  __shared__ uint32_t s_acc[kBoundThreads / 32][kBoundPerWarp][32];
+  for (uint32_t x = threadIdx.x; x < (kBoundThreads / 32) * kBoundPerWarp * 32; x += kBoundThreads)
+    (&s_acc[0][0][0])[x] = 0;
+  const uint32_t l = blockIdx.x;
+  const uint64_t c0 = max(p.loff ? p.loff[l] : l * p.stride, p.slice_lo);
+  const uint64_t c1 = min(p.loff ? p.loff[l + 1] : (l + 1) * p.stride, p.slice_hi);
+  if (c1 <= c0) return;
+  const uint32_t m = static_cast<uint32_t>(c1 - c0);
+  const uint32_t F = kF > 0 ? static_cast<uint32_t>(kF) : p.L - 1;  // left length
+  const int32_t g_lo = static_cast<int32_t>(blockIdx.y) * p.span;
+  const int32_t g_hi = min(g_lo + p.span, p.n_tiles);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr uint32_t kWarps = kBoundThreads / 32;
+  for (uint32_t r0 = 0; r0 < m; r0 += kBoundRound) {
+    const uint32_t mr = min(m - r0, static_cast<uint32_t>(kBoundRound));
+    __syncthreads();  // previous round's table reads are done
+    for (uint32_t j = tid; j < mr; j += kBoundThreads) {
+      const uint64_t cc = c0 + r0 + j;
+      s_tau[j] = p.ctypes[cc * p.L + p.L - 1];
+      const uint32_t w = p.cwin[cc * (p.L - 1) + p.L - 2];
+      uint32_t x = 0;
+      for (uint32_t a = 0; a < p.aw.n; ++a)
+        if (p.aw.w[a] == w) x = a;
+      s_widx[j] = x;
+    }
+    // this warp's candidates: j = warp + kWarps * i, i < nmine (<= 16);
+    // lane i keeps candidate i's running total
+    const uint32_t nmine = mr > warp ? (mr - warp + kWarps - 1) / kWarps : 0;
+    uint32_t acc = 0;
+    for (int32_t gc = g_lo; gc < g_hi; gc += kBoundThreads) {
+      // Phase A: dil_w(U(left)) for tile g = gc + tid, every alphabet window w
+      {
+        const int32_t g = gc + static_cast<int32_t>(tid);
+        constexpr int kU = kF > 0 ? kF + 1 : kBoundMaxL;
+        uint32_t u[kU];  // u[j] = U at tile g - F + j, j = 0..F
+        const uint32_t t0 = p.ltypes[static_cast<size_t>(l) * F];
+        // word of type t at tile g - F + j (zero outside the stream)
+        auto occ_at = [&](uint32_t t, uint32_t j) -> uint32_t {
+          const int32_t gj = g - static_cast<int32_t>(F) + static_cast<int32_t>(j);
+          return (gj >= 0 && gj < p.n_tiles) ? __ldg(p.occ + impl::occ_index(gj, t, p.blk_words)) : 0u;
+        };
+#pragma unroll
+        for (uint32_t j = 0; j < static_cast<uint32_t>(kU); ++j)
+          if (kF > 0 || j <= F) u[j] = occ_at(t0, j);
+#pragma unroll
+        for (uint32_t k = 1; k < static_cast<uint32_t>(kU) - 1; ++k) {
+          if (kF == 0 && k >= F) break;
+          const uint32_t tk = p.ltypes[static_cast<size_t>(l) * F + k];
+          const uint32_t wk = p.lwin[static_cast<size_t>(l) * (F - 1) + k - 1];
+#pragma unroll
+          for (uint32_t j = static_cast<uint32_t>(kU) - 1; j >= k; --j) {
+            if (kF > 0 || j <= F)
+              u[j] = occ_at(tk, j) &
+                     (p.uniform_w ? window_of(smear64(u[j - 1], u[j], p.sm, p.n_sm), wk) : dil_rt(wk, u[j - 1], u[j]));
+          }
+        }
+        // U(left) at tiles g-1 (u[F-1]) and g (u[F])
+        // (zero past the split: phase B then reads whole bitmap blocks)
+        const bool live = g < g_hi;
+        if (p.uniform_w) {
+          const Smear64 s = smear64(u[F - 1], u[F], p.sm, p.n_sm);
+          for (uint32_t a = 0; a < p.aw.n; ++a) D[a][tid] = live ? window_of(s, p.aw.w[a]) : 0u;
+        } else {
+          for (uint32_t a = 0; a < p.aw.n; ++a) D[a][tid] = live ? dil_rt(p.aw.w[a], u[F - 1], u[F]) : 0u;
+        }
+      }
+      __syncthreads();
+      // Phase B: lane = 4 consecutive tiles (16-byte row loads): lanes 8q..8q+7
+      // cover bitmap block q of each group of 4 blocks; D is zero past the
+      // split. Per-lane partial sums stay in shared memory (no reduction in
+      // the loop).
+      const int32_t nk = (min(kBoundThreads, g_hi - gc) + 31) >> 5;  // blocks in chunk
+      const uint32_t bw = p.blk_words;
+      const uint32_t q = lane >> 3, sub = (lane & 7) * 4;
+      const uint32_t* blk0 = p.occ + static_cast<size_t>((gc >> 5) + q) * bw + sub;
+      const uint32_t* dbase = &D[0][q * 32 + sub];
+      for (uint32_t i = 0; i < nmine; ++i) {
+        const uint32_t j = warp + kWarps * i;
+        const uint4* row = reinterpret_cast<const uint4*>(blk0 + s_tau[j] * kRowStride);
+        const uint32_t* drow = dbase + s_widx[j] * kBoundThreads;
+        uint32_t a = 0;
+#pragma unroll
+        for (int m = 0; m < kBoundThreads / 128; ++m) {
+          if (static_cast<int32_t>(q) + 4 * m < nk) {
+            const uint4 o = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(row) + 4 * m * bw));
+            const uint4 d = *reinterpret_cast<const uint4*>(drow + 128 * m);
+            a += __popc(o.x & d.x) + __popc(o.y & d.y) + __popc(o.z & d.z) + __popc(o.w & d.w);
+          }
+        }
+        s_acc[warp][i][lane] += a;
+      }
+      __syncthreads();
+    }
+    // per candidate: sum the 32 lanes' partials
+    for (uint32_t i = 0; i < nmine; ++i) {
+      uint32_t v = s_acc[warp][i][lane];
+      s_acc[warp][i][lane] = 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == i) acc = v;
+    }
+    if (lane < nmine && acc)
+      atomicAdd(p.bound + (c0 - p.slice_lo) + r0 + warp + kWarps * lane, static_cast<unsigned long long>(acc));
+  }
+}
+
+// bound < threshold prunes; the rest survive to pass 2.
+__global__ void prune_bound_kernel(const unsigned long long* __restrict__ bound, uint64_t threshold,
+                                   uint64_t n, uint64_t* counts, uint32_t* surv,
+                                   unsigned long long* pruned) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const bool keep = bound[i] >= threshold;
+  counts[i] = keep ? 0 : kPrunedDev;
+  surv[i] = keep ? 1u : 0u;
+  const unsigned ballot = __ballot_sync(__activemask(), !keep);
+  if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && ballot)
+    atomicAdd(pruned, static_cast<unsigned long long>(__popc(ballot)));
+}
+
 // Per sorted position: bound < threshold prunes, the rest survive to pass 2
 // (singleton groups are final when their relaxation is the episode itself).
 __global__ void prune_kernel(const uint32_t* __restrict__ idx_sorted, const uint32_t* __restrict__ flags,
@@ -303,12 +503,8 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   stats.episodes += n;
   uint32_t bits = 1;
   while ((1ull << bits) < stream_.alphabet + 1ull) ++bits;
-  // Pass 1 only pays when a level is large and its type sequences repeat:
-  // small levels (< kMinPass1 candidates) are cheaper to count exactly than
-  // to sort, group, count hulls and gather survivors.
-  constexpr uint64_t kMinPass1 = 16384;
   const bool grouping = mode == EPI_MODE_MINE && threshold > 1 && L >= 2 && bits * L <= 64 &&
-                        n >= kMinPass1 && n < (1ull << 31);
+                        n >= min_pass1() && n < (1ull << 31);
   if (!grouping) {
     stats.pass2_episodes += n;
     count_device(c, d_counts, stats, &stats.pass2_ms);
@@ -429,6 +625,104 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
   EPI_CUDA(cudaGetLastError());
   DevSet sv = c;
   sv.n = n;
+  sv.types = stypes;
+  sv.win = swin;
+  sv.sigma = ssigma;
+  uint64_t* sc = scratch_.get<uint64_t>(kMSurvCnt, n);
+  count_device(sv, sc, stats, &stats.pass2_ms, mslot);
+  scatter_counts_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx_out, sc, slot_ptr(mslot), d_counts);
+  EPI_CUDA(cudaGetLastError());
+  stats.kernel_launches += 2;
+}
+
+// Pass 1 by the popcount bound (bound_kernel) over the left-grouped
+// candidates of one mining level, then pass 2 on the survivors. The host does
+// not wait: survivors are sized on the device.
+void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t threshold,
+                                   const uint32_t* alpha, uint32_t n_alpha, uint64_t* d_counts,
+                                   epi_stats& stats) {
+  const uint64_t n = c.n;
+  const uint32_t L = c.N, M = L - 1;
+  stats.episodes += n;
+  stats.pass1_groups += n;
+  unsigned long long* bound = scratch_.get<unsigned long long>(kMBound, n);
+  EPI_CUDA(cudaMemsetAsync(bound, 0, n * sizeof(unsigned long long), st_));
+  BoundLaunch b{};
+  b.occ = stream_.d_occ;
+  b.blk_words = stream_.blk_words;
+  b.n_tiles = static_cast<int32_t>(stream_.n_tiles);
+  b.L = L;
+  b.ltypes = lf.types;
+  b.lwin = lf.win;
+  b.loff = lf.off;
+  b.stride = lf.stride;
+  b.ctypes = c.types - lf.slice_lo * L;  // the kernel indexes candidates globally
+  b.cwin = c.win - lf.slice_lo * M;
+  for (uint32_t a = 0; a < n_alpha; ++a) b.aw.w[a] = alpha[a];
+  b.aw.n = n_alpha;
+  b.slice_lo = lf.slice_lo;
+  b.slice_hi = lf.slice_lo + n;
+  // equal-width alphabet: one shared smear per tile instead of one per window
+  uint32_t uw = n_alpha ? (alpha[0] >> 16) - (alpha[0] & 0xffffu) + 1 : 0;
+  for (uint32_t a = 0; a < n_alpha; ++a)
+    if ((alpha[a] >> 16) - (alpha[a] & 0xffffu) + 1 != uw) uw = 0;
+  b.uniform_w = uw;
+  {
+    uint32_t cover = 1;
+    b.n_sm = 0;
+    for (int i = 0; i < 5; ++i) {
+      const uint32_t s = cover < uw ? std::min(cover, uw - cover) : 0u;
+      b.sm[i] = s;
+      cover += s;
+      if (s) b.n_sm = static_cast<uint32_t>(i + 1);
+    }
+  }
+  b.bound = bound;
+  // split time so that lefts x splits fill the GPU a few times over
+  const int64_t chunks = (static_cast<int64_t>(stream_.n_tiles) + kBoundThreads - 1) / kBoundThreads;
+  const int64_t want = std::max<int64_t>(1, (static_cast<int64_t>(num_sms_) * 8 + lf.nf - 1) / lf.nf);
+  // (<= 2^26 tiles per split keeps the u32 per-lane sums exact)
+  const int64_t splits = std::clamp<int64_t>(std::max<int64_t>(want, (stream_.n_tiles >> 26) + 1), 1,
+                                             std::max<int64_t>(chunks, 1));
+  b.span = static_cast<int32_t>((chunks + splits - 1) / splits * kBoundThreads);
+  const int64_t ysplits = (static_cast<int64_t>(stream_.n_tiles) + b.span - 1) / b.span;
+  Timed t{next_event(), nullptr, next_event(), &stats.pass1_ms, -1, n, 0, false};
+  t.e_map = t.e1;
+  EPI_CUDA(cudaEventRecord(t.e0, st_));
+  const dim3 grid(static_cast<unsigned>(lf.nf), static_cast<unsigned>(std::max<int64_t>(ysplits, 1)));
+  switch (L - 1) {
+    case 1: bound_kernel<1><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    case 2: bound_kernel<2><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    case 3: bound_kernel<3><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    case 4: bound_kernel<4><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    case 5: bound_kernel<5><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    case 6: bound_kernel<6><<<grid, kBoundThreads, 0, st_>>>(b); break;
+    default: bound_kernel<0><<<grid, kBoundThreads, 0, st_>>>(b); break;
+  }
+  EPI_CUDA(cudaGetLastError());
+  EPI_CUDA(cudaEventRecord(t.e1, st_));
+  timed_.push_back(t);
+
+  uint32_t* sflags = scratch_.get<uint32_t>(kMFlags, n);
+  uint32_t* sscan = scratch_.get<uint32_t>(kMScan, n);
+  prune_bound_kernel<<<blocks_for(n), 256, 0, st_>>>(bound, threshold, n, d_counts, sflags, d_acc_ + 2);
+  EPI_CUDA(cudaGetLastError());
+  const int mslot = new_slot();
+  dev_scan_total(sflags, sscan, n, mslot);
+  slot_counters_.push_back({mslot, &stats.pass2_episodes});
+  stats.kernel_launches += 5;
+  const size_t s_types = 0, s_win = align256(static_cast<size_t>(n) * L * 4),
+               s_sigma = s_win + align256(static_cast<size_t>(n) * M * 4),
+               s_idx = s_sigma + align256(n * 4ull), s_total = s_idx + align256(n * 4ull);
+  char* sbuf = scratch_.get<char>(kMSurv, s_total);
+  uint32_t* stypes = reinterpret_cast<uint32_t*>(sbuf + s_types);
+  uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
+  uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
+  uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
+  gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
+                                                swin, ssigma, sidx_out);
+  EPI_CUDA(cudaGetLastError());
+  DevSet sv = c;
   sv.types = stypes;
   sv.win = swin;
   sv.sigma = ssigma;
@@ -620,6 +914,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     uint32_t* d_win = scratch_.get<uint32_t>(kMWin, n * (L - 1));
     uint32_t* d_sigma = scratch_.get<uint32_t>(kMSigma, n);
     uint64_t* d_counts = scratch_.get<uint64_t>(kMCounts, sharded ? s * W : n);
+    PopLefts lefts;  // the join's lefts on the device (popcount pass 1)
+    lefts.nf = nf;
+    lefts.slice_lo = lo_c;
     if (level == 2) {
       const size_t up = nf + 2 * cfg.n_alpha;
       uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up * 4));
@@ -629,6 +926,8 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
       uint32_t* d = scratch_.get<uint32_t>(kMFreq, up);
       EPI_CUDA(cudaMemcpyAsync(d, h, up * 4, cudaMemcpyHostToDevice, st_));
       totals.h2d_bytes += up * 4;
+      lefts.types = d;
+      lefts.stride = static_cast<uint64_t>(nf) * cfg.n_alpha;
       gen_level2_kernel<<<blocks_for(n), 256, 0, st_>>>(d, static_cast<uint32_t>(nf), d + nf,
                                                         d + nf + cfg.n_alpha,
                                                         static_cast<uint32_t>(cfg.n_alpha), d_types,
@@ -654,6 +953,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
       char* d = scratch_.get<char>(kMJoin, o_end);
       EPI_CUDA(cudaMemcpyAsync(d, h, o_end, cudaMemcpyHostToDevice, st_));
       totals.h2d_bytes += o_end;
+      lefts.types = reinterpret_cast<const uint32_t*>(d + o_t);
+      lefts.win = reinterpret_cast<const uint32_t*>(d + o_w);
+      lefts.off = reinterpret_cast<const uint64_t*>(d + o_o);
       const unsigned blocks = static_cast<unsigned>((nf * 32 + 255) / 256);
       gen_join_kernel<<<blocks, 256, 0, st_>>>(
           L, reinterpret_cast<const uint32_t*>(d + o_t), reinterpret_cast<const uint32_t*>(d + o_w),
@@ -674,7 +976,15 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
     g_trace.mark("gen launched");
-    if (cnt_c > 0)
+    // Pass 1 by the popcount bound when the level is large enough to pay
+    // and every window fits one history word; else the hull relaxation.
+    const bool popbound = cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 && n >= min_pass1() &&
+                          amax <= 32 && cfg.n_alpha <= 16 && L <= static_cast<uint32_t>(kBoundMaxL) &&
+                          !std::getenv("EPI_PASS1_HULL");
+    if (cnt_c > 0 && popbound)
+      count_device_popbound(c, lefts, cfg.threshold, awin.data(), static_cast<uint32_t>(cfg.n_alpha),
+                            d_counts + lo_c, totals);
+    else if (cnt_c > 0)
       count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, awin.data(),
                             static_cast<uint32_t>(cfg.n_alpha), d_counts + lo_c, totals);
     g_trace.mark("count launched");

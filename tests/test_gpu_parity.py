@@ -355,3 +355,31 @@ def test_uniform_head_last_width_vs_port(ctx, seed, segments_env):
         csr = csr_of(eps)
         want = oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=4)
         np.testing.assert_array_equal(got, want, err_msg=f"seed {seed} it {it} W {W} WL {WL}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("pass1", ["popcount", "hull"])
+def test_mine_pass1_every_level_vs_reference(ctx, seed, pass1, monkeypatch):
+    """Pass 1 forced onto every level >= 2 (EPI_PASS1_MIN=1), with the
+    popcount bound (default) or the hull relaxation (EPI_PASS1_HULL): the
+    mining CSV must still equal the reference's mine() (no frequent episode
+    pruned, survivors' counts exact), up to level 5 and over several
+    constraint alphabets (mixed widths, lo > 0)."""
+    from paper_0905_2203_b200 import EventStream, MiningConfig, mine, write_mining_csv
+    monkeypatch.setenv("EPI_PASS1_MIN", "1")
+    if pass1 == "hull":
+        monkeypatch.setenv("EPI_PASS1_HULL", "1")
+    rng = np.random.default_rng(4200 + seed)
+    a = int(rng.integers(3, 8))
+    n = int(rng.integers(2000, 5000))
+    times = np.cumsum(rng.integers(0, [2, 4, 8, 3, 6, 12][seed] + 1, n)).astype(np.int64)
+    types = rng.integers(0, a, n).astype(np.uint32)
+    bins = [[(0, 5), (5, 10), (10, 15)], [(0, 4), (2, 7)], [(1, 9)], [(0, 3), (3, 6), (6, 9), (9, 12)],
+            [(0, 10), (10, 32)], [(4, 6), (0, 2), (20, 31)]][seed]
+    thr = int(max(2, n // (a * a * 3)))
+    csv_ref, cands_ref, _ = oracle.ref_mine(types, times, a, thr, bins, 5, switch_level=99, backend=0,
+                                            workers=4)
+    s = EventStream(types, times, a)
+    r = mine(s, MiningConfig(threshold=thr, constraint_alphabet=bins, max_level=5, mode=MODE_MINE), ctx=ctx)
+    assert [lv.candidates for lv in r.levels] == cands_ref, seed
+    assert write_mining_csv(r) == csv_ref, seed
