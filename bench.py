@@ -310,37 +310,64 @@ def run_ours(args, rank, world, local_rank):
     h2d = n * 12 + int(s0["h2d_bytes"])
     d2h = int(s0["d2h_bytes"])
 
-    # Roofline of the dominant kernel (segment-map automaton), per launch,
-    # from the engine's CUDA events on its own stream.
+    # Roofline of the dominant kernel, per launch, from the engine's CUDA
+    # events on its own stream. Two kernel families carry the device time:
+    #   machines_kernel (segment-map automaton; exact counts): matched-pair
+    #     model of SURVEY 8d, 1 INT32 op per (episode, event of one of its
+    #     types), against the measured LOP3+IMAD issue rate;
+    #   bound_kernel (pass 1, popcount bound): 1 POPC per (candidate, 32 ms
+    #     tile) word pair, against the measured POPC (XU pipe) issue rate.
     map_ms = sum(s["map_ms"] for s in stats)
     map_launches = sum(s["map_launches"] for s in stats)
     matched = sum(s["matched_pairs"] for s in stats)
     tiles = sum(s["tile_steps"] for s in stats)
+    bound_ms = sum(s["bound_ms"] for s in stats)
+    bound_words = sum(s["bound_words"] for s in stats)
     total_dev_ms = sum(s["total_ms"] for s in stats)
-    peak = ctypes_probe(_native, gpu)
-    achieved = matched / (map_ms * 1e-3) / 1e12 if map_ms > 0 else 0.0
-    # DRAM bytes per launch of the same kernel from the committed ncu --set
-    # full capture (profiles/roofline_traffic.json, scripts/traffic_json.py)
-    traffic, traffic_src = None, None
+    peak_int = ctypes_probe(_native, gpu, 1)
+    peak_popc = ctypes_probe(_native, gpu, 2)
+    traffic_all = {}
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
-            tj = json.load(f).get(args.config)
-        if tj:
-            traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
-    except (OSError, ValueError, KeyError):
+            traffic_all = json.load(f)
+    except (OSError, ValueError):
         pass
-    roofline = {"bound": "int32", "model": "matched pairs (SURVEY 8d): 1 int op per "
-                "(episode, event of an episode type)", "achieved": round(achieved, 4),
-                "peak": round(peak, 3), "unit": "Tops/s", "frac": round(achieved / peak, 5) if peak else None,
-                "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu)",
-                "traffic_source": traffic_src,
-                "peak_source": "epi_probe_int32 (LOP3+IMAD, measured in this run)",
-                "kernel": "machines_kernel", "launches": map_launches,
-                "avg_launch_ms": round(map_ms / max(map_launches, 1), 5),
-                "share_of_device_time": round(map_ms / total_dev_ms, 4) if total_dev_ms else None,
-                "tile_steps_per_s": tiles / (map_ms * 1e-3) if map_ms > 0 else None,
-                "dense_model_ee_per_s_kernel": (sum(s["episode_events"] for s in stats)
-                                                / (map_ms * 1e-3)) if map_ms > 0 else None}
+
+    def traffic_for(kernel):
+        tj = traffic_all.get(f"{args.config}:{kernel}") or (traffic_all.get(args.config)
+                                                            if kernel == "machines_kernel" else None)
+        return (tj["dram_bytes_per_launch"], tj["source"]) if tj else (None, None)
+
+    kernels = []
+    if map_ms > 0:
+        ach = matched / (map_ms * 1e-3) / 1e12
+        tr, src = traffic_for("machines_kernel")
+        kernels.append({"kernel": "machines_kernel", "bound": "int32",
+                        "model": "matched pairs (SURVEY 8d): 1 int op per (episode, event of an episode type)",
+                        "achieved": round(ach, 4), "peak": round(peak_int, 3), "unit": "Tops/s",
+                        "frac": round(ach / peak_int, 5) if peak_int else None,
+                        "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": src,
+                        "peak_source": "epi_probe_int32 mode 1 (LOP3+IMAD, measured in this run)",
+                        "launches": map_launches, "avg_launch_ms": round(map_ms / max(map_launches, 1), 5),
+                        "device_ms": round(map_ms, 4),
+                        "share_of_device_time": round(map_ms / total_dev_ms, 4) if total_dev_ms else None,
+                        "tile_steps_per_s": tiles / (map_ms * 1e-3),
+                        "dense_model_ee_per_s_kernel": sum(s["episode_events"] for s in stats) / (map_ms * 1e-3)})
+    if bound_ms > 0:
+        ach = bound_words / (bound_ms * 1e-3) / 1e12
+        tr, src = traffic_for("bound_kernel")
+        kernels.append({"kernel": "bound_kernel", "bound": "int32",
+                        "model": "pass-1 popcount bound: 1 POPC per (candidate, 32 ms tile) word pair",
+                        "achieved": round(ach, 4), "peak": round(peak_popc, 3), "unit": "Tops/s",
+                        "frac": round(ach / peak_popc, 5) if peak_popc else None,
+                        "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": src,
+                        "peak_source": "epi_probe_int32 mode 2 (POPC, XU pipe, measured in this run)",
+                        "device_ms": round(bound_ms, 4),
+                        "share_of_device_time": round(bound_ms / total_dev_ms, 4) if total_dev_ms else None})
+    kernels.sort(key=lambda k: -k["device_ms"])
+    roofline = dict(kernels[0]) if kernels else {"bound": "int32", "achieved": None, "peak": None,
+                                                 "unit": "Tops/s", "frac": None, "traffic": None}
+    roofline["kernels"] = kernels
 
     out = {
         "metric": "episode-events counted/sec (device-timed)",
@@ -356,7 +383,8 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
         "pass_breakdown": {k: stats[-1][k] for k in ("episodes", "pass1_groups", "pass2_episodes",
                                                       "pruned", "segments", "patches", "pass1_ms",
-                                                      "pass2_ms", "map_ms", "concat_ms", "total_ms")},
+                                                      "pass2_ms", "map_ms", "concat_ms", "bound_ms",
+                                                      "total_ms")},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_for(args, types, times, alphabet)
@@ -364,10 +392,10 @@ def run_ours(args, rank, world, local_rank):
     return out
 
 
-def ctypes_probe(native, device):
+def ctypes_probe(native, device, mode=1):
     import ctypes
     v = ctypes.c_double(0)
-    st = native.lib.epi_probe_int32(device, 1, ctypes.byref(v))
+    st = native.lib.epi_probe_int32(device, mode, ctypes.byref(v))
     return v.value if st == 0 else 0.0
 
 

@@ -76,6 +76,9 @@ typedef struct {
   double map_ms;              /* device time of the segment-map kernels        */
   double concat_ms;           /* device time of the concat walks               */
   double total_ms;            /* device time of the whole call                 */
+  uint64_t bound_words;       /* pass-1 popcount bound: (candidate, 32 ms tile)
+                                 AND-POPC word pairs                            */
+  double bound_ms;            /* device time of the pass-1 bound kernels       */
 } epi_stats;
 
 /* Context bound to one CUDA device. */
@@ -224,8 +227,8 @@ epi_status epi_generate_candidates(epi_ctx* ctx, uint64_t level, const epi_episo
                                    epi_episode_batch* out);
 
 /* INT32 issue-rate probe (roofline denominator): lane-ops/s in units of
- * 1e12 on `device`; mixed != 0 saturates both integer pipes (LOP3 + IMAD),
- * mixed == 0 the ALU pipe only (LOP3). */
+ * 1e12 on `device`; mixed == 1 saturates both integer pipes (LOP3 + IMAD),
+ * mixed == 0 the ALU pipe only (LOP3), mixed == 2 the POPC rate (XU pipe). */
 epi_status epi_probe_int32(int device, int mixed, double* tops_out);
 
 /* Build/version string (arch, kernel variants). */

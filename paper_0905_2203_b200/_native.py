@@ -38,7 +38,8 @@ class Stats(C.Structure):
                 ("episode_events", C.c_uint64), ("matched_pairs", C.c_uint64),
                 ("tile_steps", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("pass1_ms", C.c_double), ("pass2_ms", C.c_double), ("map_ms", C.c_double),
-                ("concat_ms", C.c_double), ("total_ms", C.c_double)]
+                ("concat_ms", C.c_double), ("total_ms", C.c_double),
+                ("bound_words", C.c_uint64), ("bound_ms", C.c_double)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

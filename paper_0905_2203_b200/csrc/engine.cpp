@@ -147,6 +147,7 @@ void Engine::flush_stats(epi_stats& stats) {
     const uint64_t live = t.live_slot >= 0 ? log[t.live_slot] : t.n_host;
     stats.total_ms += ms;
     if (t.ms_out) *t.ms_out += ms;
+    if (t.ms_out2) *t.ms_out2 += ms;
     if (t.map) {
       EPI_CUDA(cudaEventElapsedTime(&map_ms, t.e0, t.e_map));
       stats.map_ms += map_ms;
@@ -378,6 +379,20 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const int64_t max_p = std::clamp<int64_t>(tiles4 / min_seg, 1, kMaxWalkSegments);
   int64_t P = 1;
   double best = 1e300;
+  // Latency regime: the launch cannot fill the SMs even at the largest P,
+  // or its live size is known only on the device (pass-2 survivors, usually
+  // few). One warp per SM runs a tile step in ~2 walk-step latencies' time:
+  // minimise per + 2 P instead.
+  if (live_slot >= 0 || ctas_x * max_p <= num_sms_) {
+    for (int64_t cand = 1; cand <= max_p; ++cand) {
+      const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
+      const double cost = per + (cand > 1 ? 2.0 * static_cast<double>(cand) : 0.0);
+      if (cost < best * 0.999) {
+        best = cost;
+        P = cand;
+      }
+    }
+  } else
   for (int64_t cand = 1; cand <= max_p; ++cand) {
     const int64_t ctas = ctas_x * cand;
     const double rounds = static_cast<double>((ctas + num_sms_ - 1) / num_sms_);

@@ -162,6 +162,7 @@ class Engine {
     uint64_t n_host;
     uint64_t tiles_per_ep;
     bool map;             // automaton launch (map_ms / concat_ms split)
+    double* ms_out2 = nullptr;  // a second accumulator of the interval
   };
   struct SlotCounter {
     int slot;

@@ -688,6 +688,8 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   const int64_t ysplits = (static_cast<int64_t>(stream_.n_tiles) + b.span - 1) / b.span;
   Timed t{next_event(), nullptr, next_event(), &stats.pass1_ms, -1, n, 0, false};
   t.e_map = t.e1;
+  t.ms_out2 = &stats.bound_ms;
+  stats.bound_words += n * static_cast<uint64_t>(stream_.n_tiles);
   EPI_CUDA(cudaEventRecord(t.e0, st_));
   const dim3 grid(static_cast<unsigned>(lf.nf), static_cast<unsigned>(std::max<int64_t>(ysplits, 1)));
   switch (L - 1) {

@@ -35,6 +35,27 @@ __global__ void __launch_bounds__(256) int32_probe_kernel(uint32_t seed, uint32_
   if (x == 0x12345678u) sink[0] = x;
 }
 
+// POPC issue rate (XU pipe): the denominator of the pass-1 bound kernel
+// (one POPC per candidate per 32 ms tile word). Each chain step is one POPC
+// fed through one LOP3 (ALU pipe, not the bottleneck); POPCs are counted.
+__global__ void __launch_bounds__(256) popc_probe_kernel(uint32_t seed, uint32_t* sink) {
+  uint32_t a[kChains];
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) a[c] = seed * (threadIdx.x + c + 1);
+  for (int i = 0; i < kProbeIters; ++i) {
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+      uint32_t t;
+      asm volatile("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(t) : "r"(a[c]), "r"(seed), "r"(i));
+      asm volatile("popc.b32 %0, %1;" : "=r"(a[c]) : "r"(t));
+    }
+  }
+  uint32_t x = 0;
+#pragma unroll
+  for (int c = 0; c < kChains; ++c) x ^= a[c];
+  if (x == 0x12345678u) sink[0] = x;
+}
+
 }  // namespace
 }  // namespace epi
 
@@ -50,7 +71,9 @@ extern "C" epi_status epi_probe_int32(int device, int mixed, double* tops_out) {
     EPI_CUDA(cudaEventCreate(&e1));
     const int blocks = sms * 8;
     auto launch = [&] {
-      if (mixed)
+      if (mixed == 2)
+        epi::popc_probe_kernel<<<blocks, 256>>>(0x9e3779b9u, sink);
+      else if (mixed)
         epi::int32_probe_kernel<true><<<blocks, 256>>>(0x9e3779b9u, sink);
       else
         epi::int32_probe_kernel<false><<<blocks, 256>>>(0x9e3779b9u, sink);
@@ -67,7 +90,7 @@ extern "C" epi_status epi_probe_int32(int device, int mixed, double* tops_out) {
       EPI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       if (ms < best) best = ms;
     }
-    const double ops = static_cast<double>(blocks) * 256 * epi::kProbeIters * epi::kChains * 2;
+    const double ops = static_cast<double>(blocks) * 256 * epi::kProbeIters * epi::kChains * (mixed == 2 ? 1 : 2);
     *tops_out = ops / (best * 1e-3) / 1e12;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

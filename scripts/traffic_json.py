@@ -9,8 +9,12 @@ import sys
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 out = {}
-for cfg, rep, summary in [("cfg2", "gpurun_out/prof_cfg2.ncu-rep", "profiles/r01_cfg2_machines_kernel_ncu.txt"),
-                          ("cfg3", "gpurun_out/prof_cfg3.ncu-rep", "profiles/r01_cfg3_machines_kernel_ncu.txt")]:
+CAPTURES = [
+    ("cfg2:machines_kernel", "gpurun_out/prof_cfg2.ncu-rep", "profiles/r01_cfg2_machines_kernel_ncu.txt"),
+    ("cfg2:bound_kernel", "gpurun_out/prof_bound.ncu-rep", "profiles/r01_cfg2_bound_kernel_ncu.txt"),
+    ("cfg3:machines_kernel", "gpurun_out/prof_cfg3.ncu-rep", "profiles/r01_cfg3_machines_kernel_ncu.txt"),
+]
+for cfg, rep, summary in CAPTURES:
     try:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))

@@ -109,3 +109,32 @@ def test_sharded_callback_failure_is_enccl():
     with pytest.raises(EpisodicError, match="all-gather"):
         c.mine_raw(250, BINS, 3, MODE_MINE, shard=(0, 2, 16, lambda *a: 1))
     c.close()
+
+
+def test_allgather_callback_nccl_plumbing():
+    """make_allgather(memory="cuda") on hardware: device pointers wrapped as
+    torch tensors (__cuda_array_interface__), NCCL all_gather_into_tensor
+    enqueued on the engine's stream (ExternalStream). World 1 (one GPU per
+    gpurun box): recv must equal send, ordered on that stream."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+    from paper_0905_2203_b200.shard import make_allgather
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        fn = make_allgather(memory="cuda", device=torch.device("cuda", 0))
+        st = torch.cuda.Stream()
+        send = torch.arange(1000, dtype=torch.int64, device="cuda") * 7
+        recv = torch.zeros(1000, dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        assert fn(send.data_ptr(), recv.data_ptr(), 8000, st.cuda_stream) == 0
+        st.synchronize()
+        assert torch.equal(send, recv)
+    finally:
+        dist.destroy_process_group()
