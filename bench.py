@@ -15,7 +15,10 @@ every generated candidate, pruned or not (the reference counts them all).
          (12 B/event H2D + device validation/bitmap build) + epi_mine (which
          returns counts to the host) every step.
 
---config cfg1|cfg3 selects the other single-GPU configs (counting only).
+--config cfg1|cfg3|cfg4|cfg5 selects the other single-GPU configs (exact
+counting only): cfg4 = MEA-shaped bursty stream (60 electrodes, ~100M
+events) x 10,002 5-node candidates; cfg5 = one cell of the sweep
+(--cfg5-events, --cfg5-cands: 64 types at 20 Hz, random 3-node candidates).
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 compiled from /root/reference) on the host cores instead.
 """
@@ -49,6 +52,47 @@ def make_config(name):
     if name == "cfg3":
         return GenConfig(64, 7813, 20, [], 3)
     raise SystemExit(f"unknown config {name}")
+
+
+def make_stream(name, cfg5_events=10_000_000):
+    """(types, times, alphabet) of a bench config; synthetic, seeded."""
+    from paper_0905_2203_b200 import (BurstConfig, Embedding, Episode, GenConfig, generate_arrays,
+                                      generate_bursty_arrays)
+    if name == "cfg4":
+        # MEA-culture-shaped (SURVEY 8d config 4): 60 electrodes, lognormal
+        # rates, network bursts, two embedded 5-node chains; ~100M events
+        t, tm = generate_bursty_arrays(BurstConfig(electrodes=60, duration_s=175_000, seed=4,
+                                                   embedded=[Embedding(c, 0.5) for c in CFG4_CHAINS()]))
+        return t, tm, 60
+    if name == "cfg5":
+        t, tm = generate_arrays(GenConfig(64, cfg5_events / (64 * 20), 20, [], 5 + cfg5_events))
+        return t, tm, 64
+    t, tm = generate_arrays(make_config(name))
+    return t, tm, 64 if name == "cfg3" else 26
+
+
+def CFG4_CHAINS():
+    from paper_0905_2203_b200 import Episode
+    return [Episode([0, 7, 13, 21, 33], [(5, 10), (0, 5), (10, 15), (5, 10)]),
+            Episode([40, 41, 42, 43, 44], [(0, 5)] * 4)]
+
+
+def random_candidates(seed, count, alphabet, nodes):
+    rng = np.random.default_rng(seed)
+    return [([int(x) for x in rng.integers(0, alphabet, nodes)],
+             [BINS[int(b)] for b in rng.integers(0, 3, nodes - 1)]) for _ in range(count)]
+
+
+def count_candidates(name, cfg5_cands=10000):
+    if name == "cfg1":
+        return cfg1_candidates()
+    if name == "cfg3":
+        return cfg3_candidates()
+    if name == "cfg4":
+        return random_candidates(44, 10000, 60, 5) + [(c.types, c.constraints) for c in CFG4_CHAINS()]
+    if name == "cfg5":
+        return random_candidates(55, cfg5_cands, 64, 3)
+    raise SystemExit(f"{name} is not a counting config")
 
 
 def cfg1_candidates():
@@ -190,11 +234,10 @@ def run_ours(args, rank, world, local_rank):
     # collectives on device tensors for NCCL; gloo (EPI_BENCH_BACKEND, for
     # functional runs with several ranks on one GPU) takes host tensors
     coll_dev = dev if os.environ.get("EPI_BENCH_BACKEND", "nccl") == "nccl" else None
-    types, times = generate_arrays(make_config(args.config))
+    types, times, alphabet = make_stream(args.config, args.cfg5_events)
     n = len(types)
     ctx = Context(gpu)
-    ctx.load_arrays(types, times, 26 if args.config != "cfg3" else 64)
-    alphabet = 26 if args.config != "cfg3" else 64
+    ctx.load_arrays(types, times, alphabet)
 
     # Pinned host copies for the end-to-end leg.
     h_types = torch.from_numpy(types).pin_memory()
@@ -237,7 +280,7 @@ def run_ours(args, rank, world, local_rank):
         workload = {"workload": "cfg2: Sym26 mining to level 4, 3 bins, threshold 250, two-pass",
                     "events": n, "levels": 4, "threshold": 250, "bins": BINS}
     else:
-        eps = cfg1_candidates() if args.config == "cfg1" else cfg3_candidates()
+        eps = count_candidates(args.config, args.cfg5_cands)
         csr_all = to_csr(eps)
 
         def step():
@@ -247,8 +290,9 @@ def run_ours(args, rank, world, local_rank):
             else:
                 count_sharded(csr_all, count_fn, device=coll_dev)
             return merged()
-        workload = {"workload": f"{args.config}: exact counts of {len(eps)} candidates",
-                    "events": n, "candidates": len(eps)}
+        workload = {"workload": f"{args.config}: exact counts of {len(eps)} "
+                                f"{len(eps[0][0])}-node candidates",
+                    "events": n, "candidates": len(eps), "alphabet": alphabet}
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -408,18 +452,20 @@ def cpu_baseline_for(args, types, times, alphabet):
     elif args.config == "cfg1":
         csr = to_csr(cfg1_candidates())
         sample = f"all 676 cfg1 candidates x {len(types)} events"
-    else:
+    elif args.config == "cfg3":
         csr = to_csr(cfg3_candidates(64))
         sample = f"first 64 cfg3 candidates x {len(types)} events"
+    else:
+        k = 16 if len(types) > 50_000_000 else 64
+        csr = to_csr(count_candidates(args.config, args.cfg5_cands)[:k])
+        sample = f"first {k} {args.config} candidates x {len(types)} events"
     rate, kind, cores, reps, secs = cpu_reference_rate(types, times, alphabet, csr, args.cpu_seconds)
     return {"value": rate, "unit": "episode-events/s", "cores": cores, "kind": kind,
             "sample": f"{sample}; {reps} reps in {secs:.1f} s", "cpu": model}
 
 
 def run_reference(args):
-    from paper_0905_2203_b200 import generate_arrays
-    types, times = generate_arrays(make_config(args.config))
-    alphabet = 64 if args.config == "cfg3" else 26
+    types, times, alphabet = make_stream(args.config, args.cfg5_events)
     cores, model = cpu_info()
     if args.config == "cfg2":
         csr, n3 = level3_sample(types, times, 20000)
@@ -427,9 +473,13 @@ def run_reference(args):
     elif args.config == "cfg1":
         csr = to_csr(cfg1_candidates())
         sample = "all 676 cfg1 candidates"
-    else:
+    elif args.config == "cfg3":
         csr = to_csr(cfg3_candidates(64))
         sample = "first 64 cfg3 candidates"
+    else:
+        k = 16 if len(types) > 50_000_000 else 64
+        csr = to_csr(count_candidates(args.config, args.cfg5_cands)[:k])
+        sample = f"first {k} {args.config} candidates"
     for _ in range(args.warmup):
         cpu_reference_rate(types, times, alphabet, csr, 0.0)
     rates = []
@@ -459,7 +509,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--cfg5-events", type=int, default=10_000_000, help="cfg5 cell: stream length")
+    ap.add_argument("--cfg5-cands", type=int, default=10_000, help="cfg5 cell: 3-node candidates")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

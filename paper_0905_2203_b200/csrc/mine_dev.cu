@@ -14,6 +14,7 @@
 //      bound < threshold; singleton groups are already exact;
 //   3. pass 2: gather the survivors, count them exactly, scatter back;
 //   4. flag count >= threshold, compact in candidate order, copy back.
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -201,6 +202,84 @@ __global__ void hull_kernel(const uint32_t* __restrict__ types, const uint32_t* 
   }
   rsigma[g] = sig;
   gsize[g] = j1 - j0;
+}
+
+// ---- single-CTA flag / scan / compact ---------------------------------------
+// Levels of up to kOneBlkMax candidates compact in ONE launch (one CTA: each
+// thread owns a contiguous range, one block scan of the per-thread counts,
+// ranges are emitted in index order) instead of flag + two-kernel device scan
+// + total + compact: the mining levels are launch-latency bound.
+constexpr int kOneBlk = 1024;
+constexpr uint64_t kOneBlkMax = 1ull << 14;  // beyond, the multi-CTA path is faster
+
+template <class Pred, class Emit>
+__device__ __forceinline__ void one_block_compact(uint64_t n, Pred&& pred, Emit&& emit, uint32_t* total_slot,
+                                                  uint32_t* host_total) {
+  using BS = cub::BlockScan<uint32_t, kOneBlk>;
+  __shared__ typename BS::TempStorage ts;
+  const uint64_t chunk = (n + kOneBlk - 1) / kOneBlk;
+  const uint64_t b = min(n, threadIdx.x * chunk), e = min(n, b + chunk);
+  uint32_t cnt = 0;
+  for (uint64_t i = b; i < e; ++i) cnt += pred(i) ? 1u : 0u;
+  uint32_t off = 0, total = 0;
+  BS(ts).ExclusiveSum(cnt, off, total);
+  for (uint64_t i = b; i < e; ++i)
+    if (pred(i)) emit(i, off++);
+  if (threadIdx.x == 0) {
+    *total_slot = total;
+    if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
+  }
+}
+
+// count >= threshold (never the PRUNED sentinel) -> compacted frequent set
+__global__ void __launch_bounds__(kOneBlk) compact_freq_1blk(const uint64_t* __restrict__ counts,
+                                                             uint64_t threshold, uint64_t n, uint32_t L,
+                                                             const uint32_t* __restrict__ types,
+                                                             const uint32_t* __restrict__ win, uint32_t* otypes,
+                                                             uint32_t* owin, uint64_t* ocounts, uint32_t* slot,
+                                                             uint32_t* host_k) {
+  one_block_compact(
+      n,
+      [&](uint64_t i) {
+        const uint64_t x = counts[i];
+        return x != kPrunedDev && x >= threshold;
+      },
+      [&](uint64_t i, uint32_t o) {
+        for (uint32_t k = 0; k < L; ++k) otypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) owin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
+        ocounts[o] = counts[i];
+      },
+      slot, host_k);
+}
+
+// pass-1 bound < threshold prunes (PRUNED sentinel); survivors gathered
+__global__ void __launch_bounds__(kOneBlk) prune_gather_1blk(const unsigned long long* __restrict__ bound,
+                                                             uint64_t threshold, uint64_t n, uint32_t L,
+                                                             const uint32_t* __restrict__ types,
+                                                             const uint32_t* __restrict__ win,
+                                                             const uint32_t* __restrict__ sigma, uint64_t* counts,
+                                                             uint32_t* stypes, uint32_t* swin, uint32_t* ssigma,
+                                                             uint32_t* sidx, uint32_t* slot,
+                                                             unsigned long long* pruned) {
+  uint32_t np = 0;
+  one_block_compact(
+      n,
+      [&](uint64_t i) { return bound[i] >= threshold; },
+      [&](uint64_t i, uint32_t o) {
+        for (uint32_t k = 0; k < L; ++k) stypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) swin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
+        ssigma[o] = sigma[i];
+        sidx[o] = static_cast<uint32_t>(i);
+      },
+      slot, nullptr);
+  const uint64_t chunk = (n + kOneBlk - 1) / kOneBlk;
+  const uint64_t b = min(n, threadIdx.x * chunk), e = min(n, b + chunk);
+  for (uint64_t i = b; i < e; ++i) {
+    const bool keep = bound[i] >= threshold;
+    counts[i] = keep ? 0 : kPrunedDev;
+    np += keep ? 0u : 1u;
+  }
+  if (np) atomicAdd(pruned, static_cast<unsigned long long>(np));
 }
 
 // ---- pass 1, popcount bound ------------------------------------------------
@@ -705,14 +784,8 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   EPI_CUDA(cudaEventRecord(t.e1, st_));
   timed_.push_back(t);
 
-  uint32_t* sflags = scratch_.get<uint32_t>(kMFlags, n);
-  uint32_t* sscan = scratch_.get<uint32_t>(kMScan, n);
-  prune_bound_kernel<<<blocks_for(n), 256, 0, st_>>>(bound, threshold, n, d_counts, sflags, d_acc_ + 2);
-  EPI_CUDA(cudaGetLastError());
   const int mslot = new_slot();
-  dev_scan_total(sflags, sscan, n, mslot);
   slot_counters_.push_back({mslot, &stats.pass2_episodes});
-  stats.kernel_launches += 5;
   const size_t s_types = 0, s_win = align256(static_cast<size_t>(n) * L * 4),
                s_sigma = s_win + align256(static_cast<size_t>(n) * M * 4),
                s_idx = s_sigma + align256(n * 4ull), s_total = s_idx + align256(n * 4ull);
@@ -721,9 +794,22 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
   uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
   uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
-  gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
-                                                swin, ssigma, sidx_out);
-  EPI_CUDA(cudaGetLastError());
+  if (n <= kOneBlkMax) {
+    prune_gather_1blk<<<1, kOneBlk, 0, st_>>>(bound, threshold, n, L, c.types, c.win, c.sigma, d_counts,
+                                              stypes, swin, ssigma, sidx_out, slot_ptr(mslot), d_acc_ + 2);
+    EPI_CUDA(cudaGetLastError());
+    stats.kernel_launches += 3;
+  } else {
+    uint32_t* sflags = scratch_.get<uint32_t>(kMFlags, n);
+    uint32_t* sscan = scratch_.get<uint32_t>(kMScan, n);
+    prune_bound_kernel<<<blocks_for(n), 256, 0, st_>>>(bound, threshold, n, d_counts, sflags, d_acc_ + 2);
+    EPI_CUDA(cudaGetLastError());
+    dev_scan_total(sflags, sscan, n, mslot);
+    gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
+                                                  swin, ssigma, sidx_out);
+    EPI_CUDA(cudaGetLastError());
+    stats.kernel_launches += 6;
+  }
   DevSet sv = c;
   sv.types = stypes;
   sv.win = swin;
@@ -1000,26 +1086,35 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     }
 
     // ---- threshold + compaction in candidate order, straight to host -----
-    uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
-    uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
-    freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(d_counts, cfg.threshold, n, flags);
-    EPI_CUDA(cudaGetLastError());
     map_small_.get(64);
     uint32_t* h_k = static_cast<uint32_t*>(map_small_.p) + 1;
-    dev_scan_total(flags, scan, n, new_slot(), h_k);
     const size_t o_t = 0, o_w = align256(static_cast<size_t>(n) * L * 4),
                  o_c = o_w + align256(static_cast<size_t>(n) * (L - 1) * 4), o_end = o_c + align256(n * 8ull);
     map_out_.get(o_end);
     char* dm = static_cast<char*>(map_out_.d);
-    compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
-        flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(dm + o_t),
-        reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c));
-    EPI_CUDA(cudaGetLastError());
+    if (n <= kOneBlkMax) {
+      compact_freq_1blk<<<1, kOneBlk, 0, st_>>>(d_counts, cfg.threshold, n, L, d_types, d_win,
+                                                reinterpret_cast<uint32_t*>(dm + o_t),
+                                                reinterpret_cast<uint32_t*>(dm + o_w),
+                                                reinterpret_cast<uint64_t*>(dm + o_c), slot_ptr(new_slot()), h_k);
+      EPI_CUDA(cudaGetLastError());
+      totals.kernel_launches += 1;
+    } else {
+      uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
+      uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
+      freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(d_counts, cfg.threshold, n, flags);
+      EPI_CUDA(cudaGetLastError());
+      dev_scan_total(flags, scan, n, new_slot(), h_k);
+      compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
+          flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(dm + o_t),
+          reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c));
+      EPI_CUDA(cudaGetLastError());
+      totals.kernel_launches += 5;
+    }
     g_trace.mark("compact launched");
     prefetch_stats();
     EPI_CUDA(cudaStreamSynchronize(st_));
     g_trace.mark("level synced");
-    totals.kernel_launches += 5;
     const uint32_t k = *reinterpret_cast<volatile uint32_t*>(h_k);
     const char* hm = static_cast<const char*>(map_out_.p);
     std::vector<uint32_t> ntypes(static_cast<size_t>(k) * L), nwin(static_cast<size_t>(k) * (L - 1));
