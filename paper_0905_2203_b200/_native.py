@@ -41,8 +41,12 @@ class Stats(C.Structure):
                 ("concat_ms", C.c_double), ("total_ms", C.c_double),
                 ("bound_words", C.c_uint64), ("bound_ms", C.c_double)]
 
+    _names = None
+
     def as_dict(self) -> dict:
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        names = Stats._names or [name for name, _ in self._fields_]
+        Stats._names = names
+        return {name: getattr(self, name) for name in names}
 
 
 class MineConfig(C.Structure):
@@ -124,6 +128,15 @@ def ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
+def copy_out(p, count: int, dtype) -> np.ndarray:
+    """Copy `count` elements from a library-owned pointer into a new array
+    (memmove: no per-call ctypes array type as with np.ctypeslib.as_array)."""
+    out = np.empty(count, dtype=dtype)
+    if count:
+        C.memmove(out.ctypes.data, p, count * out.itemsize)
+    return out
+
+
 class CSR:
     """Episode batch in the C-ABI's CSR layout, kept alive with its arrays."""
 
@@ -145,13 +158,11 @@ class CSR:
         if n == 0:
             return CSR(np.zeros(1, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64),
                        np.zeros(0, np.int64))
-        off = np.ctypeslib.as_array(b.offsets, shape=(n + 1,)).copy()
+        off = copy_out(b.offsets, n + 1, np.uint32)
         nt = int(off[-1])
-        types = np.ctypeslib.as_array(b.types, shape=(nt,)).copy() if nt else np.zeros(0, np.uint32)
         nc = nt - n
-        low = np.ctypeslib.as_array(b.low, shape=(nc,)).copy() if nc else np.zeros(0, np.int64)
-        high = np.ctypeslib.as_array(b.high, shape=(nc,)).copy() if nc else np.zeros(0, np.int64)
-        return CSR(off, types, low, high)
+        return CSR(off, copy_out(b.types, nt, np.uint32), copy_out(b.low, nc, np.int64),
+                   copy_out(b.high, nc, np.int64))
 
     def episode(self, e: int):
         b, en = int(self.offsets[e]), int(self.offsets[e + 1])

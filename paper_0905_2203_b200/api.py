@@ -310,12 +310,11 @@ class Context:
             sh = N.Shard(int(rank), int(world), int(min_shard), cb, None)
             self._check(N.lib.epi_mine_sharded(self._h, C.byref(cfg), C.byref(sh), C.byref(res)))
         nl = int(res.n_levels)
-        cands = [int(res.level_candidates[i]) for i in range(nl)]
-        offs = [int(res.level_offsets[i]) for i in range(nl + 1)]
-        ms = [float(res.level_ms[i]) for i in range(nl)]
+        cands = N.copy_out(res.level_candidates, nl, np.uint64).tolist()
+        offs = N.copy_out(res.level_offsets, nl + 1, np.uint64).tolist()
+        ms = N.copy_out(res.level_ms, nl, np.float64).tolist()
         csr = N.CSR.from_struct(res.frequent)
-        nf = len(csr)
-        counts = np.ctypeslib.as_array(res.counts, shape=(nf,)).copy() if nf else np.zeros(0, np.uint64)
+        counts = N.copy_out(res.counts, len(csr), np.uint64)
         return cands, offs, ms, csr, counts, res.totals.as_dict()
 
 

@@ -868,16 +868,17 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
 
   auto record_level = [&](size_t cands, uint32_t L, const uint32_t* t, const uint32_t* w,
                           const uint64_t* cnt, size_t k, double ms) {
-    for (size_t i = 0; i < k; ++i) {
-      m_counts_.push_back(cnt[i]);
-      m_types_.insert(m_types_.end(), t + i * L, t + (i + 1) * L);
-      for (uint32_t j = 0; j + 1 < L; ++j) {
-        const uint32_t x = w[i * (L - 1) + j];
-        m_lo_.push_back(static_cast<int64_t>(x & 0xffff) - 1);
-        m_hi_.push_back(static_cast<int64_t>(x >> 16));
-      }
-      m_off_.push_back(static_cast<uint32_t>(m_types_.size()));
+    const size_t c0 = m_counts_.size(), t0 = m_types_.size(), w0 = m_lo_.size();
+    m_counts_.insert(m_counts_.end(), cnt, cnt + k);
+    m_types_.insert(m_types_.end(), t, t + k * L);
+    m_lo_.resize(w0 + k * (L - 1));
+    m_hi_.resize(w0 + k * (L - 1));
+    for (size_t j = 0; j < k * (L - 1); ++j) {
+      m_lo_[w0 + j] = static_cast<int64_t>(w[j] & 0xffff) - 1;
+      m_hi_[w0 + j] = static_cast<int64_t>(w[j] >> 16);
     }
+    m_off_.resize(c0 + k + 1);
+    for (size_t i = 0; i < k; ++i) m_off_[c0 + i + 1] = static_cast<uint32_t>(t0 + (i + 1) * L);
     m_level_cands_.push_back(cands);
     m_level_off_.push_back(m_counts_.size());
     m_level_ms_.push_back(ms);
@@ -943,18 +944,40 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
           for (uint32_t j = 0; j + 1 < K; ++j) k = (k << wbits) | widx(fwin[i * (F - 1) + first + j]);
           return k;
         };
-        std::vector<std::pair<uint64_t, uint32_t>> pk(nf);
-        for (size_t i = 0; i < nf; ++i) pk[i] = {key(i, 0), static_cast<uint32_t>(i)};
-        std::sort(pk.begin(), pk.end());  // (key, index): ties keep frequent order
-        g_trace.mark("join sort");
-        for (size_t i = 0; i < nf; ++i) pre[i] = pk[i].second;
-        for (uint32_t l = 0; l < nf; ++l) {
-          const uint64_t k = key(l, 1);
-          auto lo = std::lower_bound(pk.begin(), pk.end(), std::make_pair(k, 0u));
-          auto hi = std::upper_bound(lo, pk.end(), std::make_pair(k, UINT32_MAX));
-          lrange[2 * l] = static_cast<uint32_t>(lo - pk.begin());
-          lrange[2 * l + 1] = static_cast<uint32_t>(hi - pk.begin());
-          loff[l + 1] = loff[l] + (hi - lo);
+        const uint32_t kbits = K * tbits + (K > 0 ? (K - 1) * wbits : 0);
+        if (kbits <= 16) {
+          // small key space: stable counting sort, buckets read off the
+          // prefix sums (no comparison sort, no binary search)
+          std::vector<uint32_t> start((1u << kbits) + 1, 0);
+          std::vector<uint32_t> k0(nf);
+          for (size_t i = 0; i < nf; ++i) {
+            k0[i] = static_cast<uint32_t>(key(i, 0));
+            ++start[k0[i] + 1];
+          }
+          for (size_t b = 1; b < start.size(); ++b) start[b] += start[b - 1];
+          std::vector<uint32_t> fill(start.begin(), start.end() - 1);
+          for (size_t i = 0; i < nf; ++i) pre[fill[k0[i]]++] = static_cast<uint32_t>(i);
+          g_trace.mark("join sort");
+          for (uint32_t l = 0; l < nf; ++l) {
+            const uint32_t k = static_cast<uint32_t>(key(l, 1));
+            lrange[2 * l] = start[k];
+            lrange[2 * l + 1] = start[k + 1];
+            loff[l + 1] = loff[l] + (start[k + 1] - start[k]);
+          }
+        } else {
+          std::vector<std::pair<uint64_t, uint32_t>> pk(nf);
+          for (size_t i = 0; i < nf; ++i) pk[i] = {key(i, 0), static_cast<uint32_t>(i)};
+          std::sort(pk.begin(), pk.end());  // (key, index): ties keep frequent order
+          g_trace.mark("join sort");
+          for (size_t i = 0; i < nf; ++i) pre[i] = pk[i].second;
+          for (uint32_t l = 0; l < nf; ++l) {
+            const uint64_t k = key(l, 1);
+            auto lo = std::lower_bound(pk.begin(), pk.end(), std::make_pair(k, 0u));
+            auto hi = std::upper_bound(lo, pk.end(), std::make_pair(k, UINT32_MAX));
+            lrange[2 * l] = static_cast<uint32_t>(lo - pk.begin());
+            lrange[2 * l + 1] = static_cast<uint32_t>(hi - pk.begin());
+            loff[l + 1] = loff[l] + (hi - lo);
+          }
         }
       } else {
         auto cmp_key = [&](uint32_t a, uint32_t fa, uint32_t b, uint32_t fb) -> int {
