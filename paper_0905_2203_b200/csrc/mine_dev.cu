@@ -887,35 +887,13 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
   for (size_t level = 1; level <= cfg.max_level; ++level) {
     auto t0 = std::chrono::steady_clock::now();
     const uint32_t L = static_cast<uint32_t>(level);
-    if (level == 1) {
-      // Level 1: every type of the alphabet; counted on the host-set path.
-      EpisodeSet c1;
-      generate_candidates(1, EpisodeSet{}, {}, A, c1);
-      if (c1.size() == 0) break;
-      std::vector<uint64_t> counts;
-      count_set(c1, cfg.threshold, EPI_MODE_EXACT, counts, totals);
-      ftypes.clear();
-      std::vector<uint64_t> fc;
-      for (uint32_t t = 0; t < A; ++t)
-        if (counts[t] >= cfg.threshold) {
-          ftypes.push_back(t);
-          fc.push_back(counts[t]);
-        }
-      fwin.clear();
-      F = 1;
-      nf = ftypes.size();
-      record_level(A, 1, ftypes.data(), nullptr, fc.data(), nf,
-                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-      g_trace.mark("level 1 done");
-      if (nf == 0) break;
-      continue;
-    }
-
     // ---- candidate generation on the device ----------------------------
     uint64_t n = 0;
     std::vector<uint32_t> pre, lrange;
     std::vector<uint64_t> loff;
-    if (level == 2) {
+    if (level == 1) {
+      n = A;  // every type of the alphabet (E/miner.hpp:81-84)
+    } else if (level == 2) {
       n = static_cast<uint64_t>(nf) * nf * cfg.n_alpha;
     } else {
       // Join index over the frequent set: stable sort by the prefix key
@@ -1016,7 +994,8 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     if (n >= (1ull << 31)) throw Error(EPI_EUNSUPPORTED, "more than 2^31 candidates in one level");
 
     // Sharding of this level: rank R counts [R*s, R*s + cnt) of s-wide slices.
-    const bool sharded = W > 1 && n >= std::max<uint64_t>(shard->min_shard, static_cast<uint64_t>(W) * W);
+    const bool sharded =
+        level > 1 && W > 1 && n >= std::max<uint64_t>(shard->min_shard, static_cast<uint64_t>(W) * W);
     const uint64_t s = sharded ? (n + W - 1) / W : n;
     const uint64_t lo_c = sharded ? std::min<uint64_t>(static_cast<uint64_t>(R) * s, n) : 0;
     const uint64_t cnt_c = sharded ? std::min<uint64_t>(s, n - lo_c) : n;
@@ -1028,7 +1007,12 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     PopLefts lefts;  // the join's lefts on the device (popcount pass 1)
     lefts.nf = nf;
     lefts.slice_lo = lo_c;
-    if (level == 2) {
+    if (level == 1) {
+      uint32_t* h = static_cast<uint32_t*>(pin_up_.get(n * 4));
+      std::iota(h, h + n, 0u);
+      EPI_CUDA(cudaMemcpyAsync(d_types, h, n * 4, cudaMemcpyHostToDevice, st_));
+      totals.h2d_bytes += n * 4;
+    } else if (level == 2) {
       const size_t up = nf + 2 * cfg.n_alpha;
       uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up * 4));
       std::copy(ftypes.begin(), ftypes.end(), h);
@@ -1075,7 +1059,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
           reinterpret_cast<const uint64_t*>(d + o_o), d_types, d_win, d_sigma);
       EPI_CUDA(cudaGetLastError());
     }
-    totals.kernel_launches += 1;
+    if (level > 1) totals.kernel_launches += 1;
 
     DevSet c;
     c.N = L;
@@ -1092,7 +1076,12 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     const bool popbound = cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 && n >= min_pass1() &&
                           amax <= 32 && cfg.n_alpha <= 16 && L <= static_cast<uint32_t>(kBoundMaxL) &&
                           !std::getenv("EPI_PASS1_HULL");
-    if (cnt_c > 0 && popbound)
+    if (level == 1) {
+      // single-node episodes: a popcount of each type's bitmap row
+      totals.episodes += n;
+      totals.pass2_episodes += n;
+      count_device(c, d_counts, totals, &totals.pass2_ms);
+    } else if (cnt_c > 0 && popbound)
       count_device_popbound(c, lefts, cfg.threshold, awin.data(), static_cast<uint32_t>(cfg.n_alpha),
                             d_counts + lo_c, totals);
     else if (cnt_c > 0)
