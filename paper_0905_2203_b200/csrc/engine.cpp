@@ -381,12 +381,14 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   double best = 1e300;
   // Latency regime: the launch cannot fill the SMs even at the largest P,
   // or its live size is known only on the device (pass-2 survivors, usually
-  // few). One warp per SM runs a tile step in ~2 walk-step latencies' time:
-  // minimise per + 2 P instead.
+  // few). A lone warp's concat-walk step (dependent global loads, boundary
+  // patches) costs about as much as kWalkLatency of its map tile steps
+  // (measured on cfg2's small levels): minimise per + kWalkLatency * P.
+  constexpr double kWalkLatency = 12.0;
   if (live_slot >= 0 || ctas_x * max_p <= num_sms_) {
     for (int64_t cand = 1; cand <= max_p; ++cand) {
       const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
-      const double cost = per + (cand > 1 ? 2.0 * static_cast<double>(cand) : 0.0);
+      const double cost = per + (cand > 1 ? kWalkLatency * static_cast<double>(cand) : 0.0);
       if (cost < best * 0.999) {
         best = cost;
         P = cand;
