@@ -57,8 +57,11 @@ struct DeviceStream {
   int64_t* d_times_raw = nullptr;
   uint64_t raw_cap = 0;
   uint64_t launches = 0;   // kernels launched by loads (stats)
-  std::vector<uint64_t> type_hist;  // events per type (a_pad entries; matched-pair model)
-  unsigned long long* d_hist = nullptr;  // device copy of type_hist (scratch-owned)
+  std::vector<uint64_t> type_hist;  // events per type (a_pad entries), see host_hist
+  bool hist_on_host = false;
+  unsigned long long* d_hist = nullptr;  // events per type on the device (scratch-owned)
+  // Host copy of the per-type event counts (one D2H on first use per load).
+  const std::vector<uint64_t>& host_hist(cudaStream_t st);
 
   ~DeviceStream() { release(); }
   void release();

@@ -195,6 +195,7 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
     // An empty stream still gets one (zero) tile so kernels need no special case.
     ensure_occ(1, st);
     type_hist.assign(a_pad, 0);
+    hist_on_host = true;
     d_hist = scratch.get<unsigned long long>(2, a_pad);
     EPI_CUDA(cudaMemsetAsync(d_hist, 0, a_pad * sizeof(unsigned long long), st));
     n = 0;
@@ -234,13 +235,20 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
       d_types, d_times, n_events, cap, d_sums, a_pad, d_occ, d_hist, smem_hist);
   EPI_CUDA(cudaGetLastError());
   launches += 1;
-  type_hist.assign(a_pad, 0);
-  EPI_CUDA(cudaMemcpyAsync(type_hist.data(), d_hist, a_pad * sizeof(uint64_t),
-                           cudaMemcpyDeviceToHost, st));
-  EPI_CUDA(cudaStreamSynchronize(st));
+  hist_on_host = false;  // copied on demand (host_hist): no second sync per load
   n = n_events;
   n_tiles = tiles;
   span = h_total + 1;
+}
+
+const std::vector<uint64_t>& DeviceStream::host_hist(cudaStream_t st) {
+  if (!hist_on_host) {
+    type_hist.assign(a_pad, 0);
+    EPI_CUDA(cudaMemcpyAsync(type_hist.data(), d_hist, a_pad * sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    EPI_CUDA(cudaStreamSynchronize(st));
+    hist_on_host = true;
+  }
+  return type_hist;
 }
 
 void DeviceStream::ensure_occ(uint64_t tiles, cudaStream_t st) {

@@ -250,11 +250,12 @@ void Engine::ensure_type_index() {
   if (csr_valid_) return;
   const uint64_t n = stream_.n;
   const uint32_t a_pad = stream_.a_pad;
+  const std::vector<uint64_t>& hist = stream_.host_hist(st_);
   csr_off_.assign(a_pad + 1, 0);
-  for (uint32_t t = 0; t < a_pad; ++t) csr_off_[t + 1] = csr_off_[t] + stream_.type_hist[t];
+  for (uint32_t t = 0; t < a_pad; ++t) csr_off_[t + 1] = csr_off_[t] + hist[t];
   csr_cap_ = 0;
   for (uint32_t t = 0; t < a_pad; ++t)
-    csr_cap_ = std::max<uint64_t>(csr_cap_, stream_.type_hist[t]);
+    csr_cap_ = std::max<uint64_t>(csr_cap_, hist[t]);
   d_csr_off_ = scratch_.get<uint64_t>(kTCsrKeys + 100, a_pad + 1);
   EPI_CUDA(cudaMemcpyAsync(d_csr_off_, csr_off_.data(), (a_pad + 1) * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, st_));
