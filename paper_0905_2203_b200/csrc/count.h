@@ -36,6 +36,7 @@ struct CountLaunch {
   unsigned long long* patches;  // walk statistics counter
   int* occ_query;            // host: non-null -> launch_machines* reports CTAs/SM, no launch
   uint32_t last_sh[4];       // launch_machines_last: doubling-smear shifts of the last window
+  int32_t walk_warp;         // concat walk: one warp per episode (walk_warp_kernel, P <= 128)
 };
 
 // Doubling-smear shift amounts covering a window of width w (1..16).

@@ -536,6 +536,105 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   }
 }
 
+// Segment q of episode e entered in RESTART(L) (the previous segment's last
+// completion L lies inside q's window): re-run the machine from L, cleared
+// with pe = L, only until it provably coincides with the FRESH machine (same
+// completion, or both quiet for sum(high)) and read the rest of the segment
+// off the FRESH record ("patch", cf. E/mapconcat.hpp:144-148). Returns the
+// segment's count and last in-segment completion (~0 if none).
+template <int N, class Hist>
+__device__ __forceinline__ void patch_segment(const CountLaunch& p, const EpParams<N>& ep, uint32_t e,
+                                              int q, uint64_t L, uint32_t fcnt, uint64_t flast,
+                                              uint32_t& cnt, uint64_t& last) {
+  const int32_t gq = seg_bound(p, q);
+  const int32_t gn = seg_bound(p, q + 1);
+  const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
+  const uint64_t tq = static_cast<uint64_t>(gq) * 32;
+  const uint32_t nf = p.f_ncomp[idx];
+  const uint32_t nrec = nf < kRecorded ? nf : kRecorded;
+  uint64_t first[kRecorded];
+#pragma unroll
+  for (int j = 0; j < kRecorded; ++j)
+    first[j] = j < static_cast<int>(nrec) ? p.f_first[idx * kRecorded + j] : ~0ull;
+  Machine<N, Hist> m;
+  const int32_t gL = static_cast<int32_t>(L >> 5);
+  m.hist.reset(gL, p.hist_words);
+  m.set_threshold(static_cast<int64_t>(L));
+  uint32_t rc = 0;
+  uint64_t rl = ~0ull;
+  bool synced = false;
+  // Quiet-window sync: once both machines' last clear (R: its restart or
+  // last completion; F: its fresh start at the window or its last
+  // completion) lies more than sum(high) before T, every live entry at T
+  // comes from chains starting in [T - sum(high), T), which both machines
+  // hold identically, and pe no longer matters: from T on, R == F.
+  const int64_t sigma = static_cast<int64_t>(ep.sigma);
+  const int64_t f_start = static_cast<int64_t>(tq) - sigma - 1;  // F admits starts >= window
+  int64_t last_r = static_cast<int64_t>(L);
+  auto quiet = [&](int64_t T) -> bool {
+    if (last_r + sigma >= T) return false;
+    if (nf > static_cast<uint32_t>(kRecorded) && static_cast<int64_t>(first[kRecorded - 1]) < T)
+      return false;  // F completions before T not all recorded
+    int64_t last_f = f_start;
+    uint32_t f_before = 0;  // F in-segment completions before T
+#pragma unroll
+    for (int j = 0; j < kRecorded; ++j)
+      if (j < static_cast<int>(nrec) && static_cast<int64_t>(first[j]) < T) {
+        last_f = static_cast<int64_t>(first[j]);
+        if (first[j] >= tq) ++f_before;
+      }
+    if (last_f + sigma >= T) return false;
+    const uint32_t rest = fcnt - f_before;
+    cnt = rc + rest;
+    last = rest ? flast : rl;
+    return true;
+  };
+  auto on_c = [&](uint64_t tc) -> bool {
+    if (tc >= tq) {
+      ++rc;
+      rl = tc;
+    }
+    last_r = static_cast<int64_t>(tc);
+    uint32_t inseg = 0;
+#pragma unroll
+    for (int j = 0; j < kRecorded; ++j) {
+      if (j < static_cast<int>(nrec)) {
+        if (first[j] >= tq) ++inseg;
+        if (first[j] == tc) {
+          const uint32_t rest = fcnt - inseg;
+          cnt = rc + rest;
+          last = rest ? flast : rl;
+          synced = true;
+          return true;
+        }
+      }
+    }
+    return false;
+  };
+  for (int32_t g = gL; g < gn; ++g) {
+    if (g > gL && quiet(static_cast<int64_t>(g) * 32)) {
+      synced = true;
+      break;
+    }
+    uint32_t occ[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) occ[k] = __ldg(p.occ + occ_index(g, ep.type[k], p.blk_words));
+    if (tile_step<N, Hist, true>(m, ep, occ, g, p, on_c)) break;
+  }
+  if (!synced) {
+    cnt = rc;
+    last = rl;
+  }
+}
+
+// Whether segment q's successor starts in RESTART: q has an in-segment
+// completion inside the successor's window.
+__device__ __forceinline__ bool restarts_next(const CountLaunch& p, int q, uint32_t cnt, uint64_t last,
+                                              uint32_t sigma) {
+  const int64_t wn = static_cast<int64_t>(seg_bound(p, q + 1)) * 32 - static_cast<int64_t>(sigma);
+  return (q + 1 < p.P) && cnt > 0 && static_cast<int64_t>(last) >= wn;
+}
+
 // Concat step: one thread per episode chains the P segment records.
 template <int N, class Hist>
 __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
@@ -561,100 +660,104 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
         pf_last[j] = qq < p.P ? p.f_last[ix] : ~0ull;
       }
     }
-    const int32_t gq = seg_bound(p, q);
-    const int32_t gn = seg_bound(p, q + 1);
-    const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
     const uint32_t fcnt = pf_cnt[q % kPrefetch];
     const uint64_t flast = pf_last[q % kPrefetch];
     uint32_t cnt = fcnt;
     uint64_t last = flast;
     if (restart) {
       ++patches;
-      const uint64_t tq = static_cast<uint64_t>(gq) * 32;
-      const uint32_t nf = p.f_ncomp[idx];
-      const uint32_t nrec = nf < kRecorded ? nf : kRecorded;
-      uint64_t first[kRecorded];
-#pragma unroll
-      for (int j = 0; j < kRecorded; ++j)
-        first[j] = j < static_cast<int>(nrec) ? p.f_first[idx * kRecorded + j] : ~0ull;
-      Machine<N, Hist> m;
-      const int32_t gL = static_cast<int32_t>(L >> 5);
-      m.hist.reset(gL, p.hist_words);
-      m.set_threshold(static_cast<int64_t>(L));
-      uint32_t rc = 0;
-      uint64_t rl = ~0ull;
-      bool synced = false;
-      // Quiet-window sync: once both machines' last clear (R: its restart or
-      // last completion; F: its fresh start at the window or its last
-      // completion) lies more than sum(high) before T, every live entry at T
-      // comes from chains starting in [T - sum(high), T), which both machines
-      // hold identically, and pe no longer matters: from T on, R == F.
-      const int64_t sigma = static_cast<int64_t>(ep.sigma);
-      const int64_t f_start = static_cast<int64_t>(tq) - sigma - 1;  // F admits starts >= window
-      int64_t last_r = static_cast<int64_t>(L);
-      auto quiet = [&](int64_t T) -> bool {
-        if (last_r + sigma >= T) return false;
-        if (nf > static_cast<uint32_t>(kRecorded) && static_cast<int64_t>(first[kRecorded - 1]) < T)
-          return false;  // F completions before T not all recorded
-        int64_t last_f = f_start;
-        uint32_t f_before = 0;  // F in-segment completions before T
-#pragma unroll
-        for (int j = 0; j < kRecorded; ++j)
-          if (j < static_cast<int>(nrec) && static_cast<int64_t>(first[j]) < T) {
-            last_f = static_cast<int64_t>(first[j]);
-            if (first[j] >= tq) ++f_before;
-          }
-        if (last_f + sigma >= T) return false;
-        const uint32_t rest = fcnt - f_before;
-        cnt = rc + rest;
-        last = rest ? flast : rl;
-        return true;
-      };
-      auto on_c = [&](uint64_t tc) -> bool {
-        if (tc >= tq) {
-          ++rc;
-          rl = tc;
-        }
-        last_r = static_cast<int64_t>(tc);
-        uint32_t inseg = 0;
-#pragma unroll
-        for (int j = 0; j < kRecorded; ++j) {
-          if (j < static_cast<int>(nrec)) {
-            if (first[j] >= tq) ++inseg;
-            if (first[j] == tc) {
-              const uint32_t rest = fcnt - inseg;
-              cnt = rc + rest;
-              last = rest ? flast : rl;
-              synced = true;
-              return true;
-            }
-          }
-        }
-        return false;
-      };
-      for (int32_t g = gL; g < gn; ++g) {
-        if (g > gL && quiet(static_cast<int64_t>(g) * 32)) {
-          synced = true;
-          break;
-        }
-        uint32_t occ[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) occ[k] = __ldg(p.occ + occ_index(g, ep.type[k], p.blk_words));
-        if (tile_step<N, Hist, true>(m, ep, occ, g, p, on_c)) break;
-      }
-      if (!synced) {
-        cnt = rc;
-        last = rl;
-      }
+      patch_segment<N, Hist>(p, ep, e, q, L, fcnt, flast, cnt, last);
     }
     total += cnt;
-    const int64_t wn = static_cast<int64_t>(gn) * 32 - static_cast<int64_t>(ep.sigma);
-    restart = (q + 1 < p.P) && cnt > 0 && static_cast<int64_t>(last) >= wn;
+    restart = restarts_next(p, q, cnt, last, ep.sigma);
     L = last;
   }
   p.counts[e] = total;
   if (patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));
 }
+
+// Concat step, warp-parallel (few episodes, many segments): one warp per
+// episode, lane j owns segments j, j+32, ... Every segment's outcome is first
+// taken to be its FRESH record; then, in rounds, each segment whose
+// predecessor's current outcome ends inside its window is re-patched from
+// that completion, until no outcome changes (the chain's fixpoint, i.e. the
+// sequential walk's result; usually one or two rounds). The walk's latency
+// drops from P dependent steps to a few parallel rounds.
+constexpr int kWalkWarpSegs = 4;  // segments per lane (P <= 128)
+
+template <int N, class Hist>
+__device__ __forceinline__ void walk_warp_episode(const CountLaunch& p, uint32_t e, int lane) {
+  const EpParams<N> ep = load_episode<N>(p, e);
+  uint32_t fc[kWalkWarpSegs], cnt[kWalkWarpSegs];
+  uint64_t fl[kWalkWarpSegs], last[kWalkWarpSegs], from[kWalkWarpSegs];
+#pragma unroll
+  for (int i = 0; i < kWalkWarpSegs; ++i) {
+    const int q = lane + 32 * i;
+    const size_t ix = static_cast<size_t>(q) * p.n_eps + e;
+    fc[i] = q < p.P ? p.f_count[ix] : 0u;
+    fl[i] = q < p.P ? p.f_last[ix] : ~0ull;
+    cnt[i] = fc[i];
+    last[i] = fl[i];
+    from[i] = ~0ull;  // FRESH
+  }
+  uint32_t patches = 0;
+  for (int round = 0; round <= p.P; ++round) {
+    // predecessor outcome of each owned segment (segment q-1 is owned by
+    // lane (q-1) & 31, slot (q-1) >> 5)
+    bool changed = false;
+#pragma unroll
+    for (int i = 0; i < kWalkWarpSegs; ++i) {
+      const int q = lane + 32 * i;
+      const int src_lane = (lane + 31) & 31;
+      const int src_slot = lane == 0 ? i - 1 : i;
+      uint32_t pc = 0;
+      uint64_t pl = 0;
+#pragma unroll
+      for (int j = 0; j < kWalkWarpSegs; ++j) {
+        const uint32_t c_j = __shfl_sync(0xffffffffu, cnt[j], src_lane);
+        const uint64_t l_j = __shfl_sync(0xffffffffu, last[j], src_lane);
+        if (j == src_slot) {
+          pc = c_j;
+          pl = l_j;
+        }
+      }
+      const bool rs = q > 0 && q < p.P && restarts_next(p, q - 1, pc, pl, ep.sigma);
+      const uint64_t want = rs ? pl : ~0ull;
+      if (q < p.P && want != from[i]) {
+        uint32_t c2 = fc[i];
+        uint64_t l2 = fl[i];
+        if (rs) {
+          ++patches;
+          patch_segment<N, Hist>(p, ep, e, q, pl, fc[i], fl[i], c2, l2);
+        }
+        changed |= c2 != cnt[i] || l2 != last[i];
+        cnt[i] = c2;
+        last[i] = l2;
+        from[i] = want;
+      }
+    }
+    if (!__any_sync(0xffffffffu, changed)) break;
+  }
+  uint64_t total = 0;
+#pragma unroll
+  for (int i = 0; i < kWalkWarpSegs; ++i) total += cnt[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0) p.counts[e] = total;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) patches += __shfl_xor_sync(0xffffffffu, patches, o);
+  if (lane == 0 && patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));
+}
+
+template <int N, class Hist>
+__global__ void __launch_bounds__(128) walk_warp_kernel(const CountLaunch p) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  const uint32_t n_live = live_eps(p);
+  const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n_live; e += n_warps)
+    walk_warp_episode<N, Hist>(p, e, lane);
+}
+
 
 inline size_t machines_smem(const CountLaunch& p) {
   return 128 + static_cast<size_t>(p.stages) * p.blk_words * 4;
@@ -689,7 +792,14 @@ void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
 
 template <int N, class Hist>
 void launch_walk_n(const CountLaunch& p, cudaStream_t st) {
-  walk_kernel<N, Hist><<<(p.n_eps + 127) / 128, 128, 0, st>>>(p);
+  if (p.walk_warp && p.P <= 32 * kWalkWarpSegs) {
+    // one warp per live episode, grid-stride (the live count may be known
+    // only on the device)
+    const uint64_t blocks = std::min<uint64_t>((static_cast<uint64_t>(p.n_eps) * 32 + 127) / 128, 4096);
+    walk_warp_kernel<N, Hist><<<static_cast<unsigned>(blocks), 128, 0, st>>>(p);
+  } else {
+    walk_kernel<N, Hist><<<(p.n_eps + 127) / 128, 128, 0, st>>>(p);
+  }
   EPI_CUDA(cudaGetLastError());
 }
 

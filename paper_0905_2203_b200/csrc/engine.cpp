@@ -356,6 +356,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const uint32_t max_sigma = ds.max_sigma;
   const int32_t window_tiles = static_cast<int32_t>((max_sigma + 31) / 32 + 1);
   constexpr int64_t kMaxWalkSegments = 128;
+  constexpr uint64_t kWarpWalkMax = 4096;
   constexpr double kWalkStep = 20.0;
   // resident map CTAs per SM for this launch shape (cached per shape)
   const uint64_t shape = (static_cast<uint64_t>(N) << 48) ^ (static_cast<uint64_t>(ds.width) << 40) ^
@@ -384,7 +385,10 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // few). A lone warp's concat-walk step (dependent global loads, boundary
   // patches) costs about as much as kWalkLatency of its map tile steps
   // (measured on cfg2's small levels): minimise per + kWalkLatency * P.
-  constexpr double kWalkLatency = 12.0;
+  // Few episodes (or a device-sized set) walk warp-parallel: a segment costs
+  // ~2 tile steps there instead of ~12 in the sequential walk.
+  p.walk_warp = (live_slot >= 0 || n <= kWarpWalkMax) && !std::getenv("EPI_WALK_SEQ") ? 1 : 0;
+  const double kWalkLatency = p.walk_warp ? 2.0 : 12.0;
   if (live_slot >= 0 || ctas_x * max_p <= num_sms_) {
     for (int64_t cand = 1; cand <= max_p; ++cand) {
       const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
@@ -400,7 +404,8 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     const double rounds = static_cast<double>((ctas + num_sms_ - 1) / num_sms_);
     const double fill = std::min(1.0, static_cast<double>(ctas) / static_cast<double>(slots));
     const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
-    const double cost = rounds * per * (1.0 + 0.3 * (1.0 - fill)) + (cand > 1 ? kWalkStep * cand : 0.0);
+    const double cost = rounds * per * (1.0 + 0.3 * (1.0 - fill)) +
+                        (cand > 1 ? (p.walk_warp ? 4.0 : kWalkStep) * cand : 0.0);
     if (cost < best * 0.999) {
       best = cost;
       P = cand;

@@ -52,8 +52,17 @@ def test_known_answer_tests_many_segments(ctx, golden_kats, segments_env):
             assert int(got[0]) == k["expected"], (k["name"], p)
 
 
-@pytest.mark.parametrize("force", [None, 2, 5, 13])
-def test_reference_corpora(ctx, golden_instances, segments_env, force):
+@pytest.fixture(params=["warp", "seq"])
+def walk_mode(request, monkeypatch):
+    """Concat walk: warp-parallel (default for small sets) or the sequential
+    one-thread-per-episode walk (EPI_WALK_SEQ)."""
+    if request.param == "seq":
+        monkeypatch.setenv("EPI_WALK_SEQ", "1")
+    return request.param
+
+
+@pytest.mark.parametrize("force", [None, 2, 5, 13, 64])
+def test_reference_corpora(ctx, golden_instances, segments_env, force, walk_mode):
     """T/test_fsm.cpp, T/test_tracking.cpp, T/test_mapconcat.cpp,
     T/acceptance.cpp C1 corpora: device count == reference count_fsm ==
     oracle_count, at several forced segment counts (MapConcatenate
@@ -86,7 +95,7 @@ def _random_case(rng, n_max, alphabet_max, gap_max, n_nodes_max, high_max):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_random_vs_port(ctx, seed, segments_env):
+def test_random_vs_port(ctx, seed, segments_env, walk_mode):
     """Wider random instances than the reference's (windows up to 63, up to
     10 nodes, thousands of events, idle gaps that trigger time compression)
     against the oracle port (count_fsm restated)."""
