@@ -145,9 +145,16 @@ class CSR:
         self.types = np.ascontiguousarray(types, dtype=np.uint32)
         self.low = np.ascontiguousarray(low, dtype=np.int64)
         self.high = np.ascontiguousarray(high, dtype=np.int64)
-        n = len(self.offsets) - 1
-        self.struct = EpisodeBatch(n, ptr(self.offsets, C.c_uint32), ptr(self.types, C.c_uint32),
-                                   ptr(self.low, C.c_int64), ptr(self.high, C.c_int64))
+        self._struct = None
+
+    @property
+    def struct(self) -> EpisodeBatch:
+        """The C-ABI view (built on first use; it borrows this object's arrays)."""
+        if self._struct is None:
+            self._struct = EpisodeBatch(len(self.offsets) - 1, ptr(self.offsets, C.c_uint32),
+                                        ptr(self.types, C.c_uint32), ptr(self.low, C.c_int64),
+                                        ptr(self.high, C.c_int64))
+        return self._struct
 
     def __len__(self):
         return len(self.offsets) - 1

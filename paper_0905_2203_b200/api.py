@@ -290,10 +290,14 @@ class Context:
         runs epi_mine_sharded: allgather(send_ptr, recv_ptr, bytes_per_rank,
         stream_ptr) -> 0 must all-gather the per-rank count slices (see
         shard.make_allgather)."""
-        lo = np.array([b[0] for b in bins], dtype=np.int64)
-        hi = np.array([b[1] for b in bins], dtype=np.int64)
-        cfg = N.MineConfig(int(threshold), int(max_level), N.ptr(lo, C.c_int64), N.ptr(hi, C.c_int64),
-                           len(bins), int(mode))
+        key = (tuple((int(b[0]), int(b[1])) for b in bins), int(threshold), int(max_level), int(mode))
+        cached = getattr(self, "_mine_cfg", None)
+        if cached is None or cached[0] != key:
+            lo = np.array([b[0] for b in key[0]], dtype=np.int64)
+            hi = np.array([b[1] for b in key[0]], dtype=np.int64)
+            cfg_ = N.MineConfig(key[1], key[2], N.ptr(lo, C.c_int64), N.ptr(hi, C.c_int64), len(bins), key[3])
+            self._mine_cfg = cached = (key, cfg_, lo, hi)  # arrays kept alive with the struct
+        cfg = cached[1]
         res = N.MineResult()
         if shard is None:
             self._check(N.lib.epi_mine(self._h, C.byref(cfg), C.byref(res)))

@@ -149,7 +149,10 @@ void Engine::flush_stats(epi_stats& stats) {
     if (t.ms_out) *t.ms_out += ms;
     if (t.ms_out2) *t.ms_out2 += ms;
     if (t.map) {
-      EPI_CUDA(cudaEventElapsedTime(&map_ms, t.e0, t.e_map));
+      if (t.e_map == t.e1)
+        map_ms = ms;
+      else
+        EPI_CUDA(cudaEventElapsedTime(&map_ms, t.e0, t.e_map));
       stats.map_ms += map_ms;
       stats.concat_ms += ms - map_ms;
       stats.episode_events += live * stream_.n;
@@ -159,8 +162,7 @@ void Engine::flush_stats(epi_stats& stats) {
   timed_.clear();
   slot_counters_.clear();
   log_used_ = 0;
-  ev_used_ = 0;
-  EPI_CUDA(cudaMemsetAsync(d_acc_, 0, 4 * sizeof(unsigned long long), st_));
+  ev_used_ = 0;  // (begin_op zeroes the device accumulators of the next call)
 }
 
 // Host -> device through pinned staging unless the source is already pinned.
@@ -446,17 +448,19 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     const int64_t gq = q * seg_len, gn = std::min<int64_t>((q + 1) * seg_len, tiles4);
     tiles += static_cast<uint64_t>(gn - std::max<int64_t>(gq - window_tiles, 0));
   }
-  Timed t{next_event(), next_event(), next_event(), ms_out, live_slot, n, tiles, true};
+  Timed t{next_event(), next_event(), nullptr, ms_out, live_slot, n, tiles, true};
   EPI_CUDA(cudaEventRecord(t.e0, st_));
   launch_map();
   EPI_CUDA(cudaEventRecord(t.e_map, st_));
+  t.e1 = t.e_map;
   if (P > 1) {
     if (wide)
       launch_walk_wide(static_cast<int>(N), p, st_);
     else
       launch_walk(static_cast<int>(N), p, st_);
+    t.e1 = next_event();
+    EPI_CUDA(cudaEventRecord(t.e1, st_));
   }
-  EPI_CUDA(cudaEventRecord(t.e1, st_));
   timed_.push_back(t);
   stats.segments = static_cast<uint64_t>(P);
   stats.kernel_launches += P > 1 ? 3 : 2;  // matched-pair stats + map (+ walk)
