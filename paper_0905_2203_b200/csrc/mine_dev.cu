@@ -15,6 +15,7 @@
 //   3. pass 2: gather the survivors, count them exactly, scatter back;
 //   4. flag count >= threshold, compact in candidate order, copy back.
 #include <cub/block/block_scan.cuh>
+#include <cuda/atomic>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -53,6 +54,7 @@ enum MineSlot : size_t {
   kMSurvCnt,
   kMGather,    // all-gathered level counts (sharded mining)
   kMBound,     // pass-1 popcount bounds
+  kMLookback,  // tile counter + status words of the single-pass compactions
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -229,6 +231,120 @@ __device__ __forceinline__ void one_block_compact(uint64_t n, Pred&& pred, Emit&
     *total_slot = total;
     if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
   }
+}
+
+// ---- single-pass stream compaction (decoupled look-back) --------------------
+// Order-preserving flag/scan/compact of any size in ONE launch: tiles of
+// kLbTile items taken in launch order (atomic tile counter), each CTA scans
+// its tile, publishes its aggregate, looks back over its predecessors'
+// published aggregates/prefixes and emits. Replaces flag kernel + two-kernel
+// device scan + total + compact kernel (5 launches) on the mining levels.
+// state[0] is the tile counter, state[1..] the tile status words (flag in the
+// top two bits: 1 aggregate, 2 inclusive prefix); zeroed before each launch.
+constexpr int kLbThreads = 256;
+constexpr int kLbItems = 8;
+constexpr uint64_t kLbTile = static_cast<uint64_t>(kLbThreads) * kLbItems;
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbIncl = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+inline uint64_t lb_tiles(uint64_t n) { return (n + kLbTile - 1) / kLbTile; }
+
+template <class Pred, class Emit>
+__device__ __forceinline__ void lookback_compact(uint64_t n, Pred&& pred, Emit&& emit, unsigned long long* state,
+                                                 uint32_t* total_slot, uint32_t* host_total) {
+  using BS = cub::BlockScan<uint32_t, kLbThreads>;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_excl;
+  if (threadIdx.x == 0) s_tile = static_cast<uint32_t>(atomicAdd(state, 1ull));
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = static_cast<uint64_t>(tile) * kLbTile;
+  if (base >= n && tile > 0) return;  // grid sized for an upper bound of n
+  const uint64_t b = base + static_cast<uint64_t>(threadIdx.x) * kLbItems;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j)
+    if (b + j < n && pred(b + j)) bits |= 1u << j;
+  uint32_t off = 0, agg = 0;
+  BS(ts).ExclusiveSum(static_cast<uint32_t>(__popc(bits)), off, agg);
+  if (threadIdx.x == 0) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(state[1 + tile]);
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      me.store(kLbIncl | agg, cuda::memory_order_release);
+    } else {
+      me.store(kLbAgg | agg, cuda::memory_order_release);
+      for (uint32_t t = tile; t-- > 0;) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(state[1 + t]);
+        unsigned long long v;
+        while (((v = st.load(cuda::memory_order_acquire)) >> 62) == 0) {
+        }
+        excl += v & kLbVal;
+        if ((v >> 62) == 2) break;
+      }
+      me.store(kLbIncl | (excl + agg), cuda::memory_order_release);
+    }
+    s_excl = excl;
+    if (base + kLbTile >= n) {  // the last tile knows the total
+      const uint32_t total = static_cast<uint32_t>(excl + agg);
+      *total_slot = total;
+      if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
+    }
+  }
+  __syncthreads();
+  uint64_t o = s_excl + off;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j)
+    if (bits & (1u << j)) emit(b + j, o++);
+}
+
+__global__ void __launch_bounds__(kLbThreads) compact_freq_lb(const uint64_t* __restrict__ counts,
+                                                              uint64_t threshold, uint64_t n, uint32_t L,
+                                                              const uint32_t* __restrict__ types,
+                                                              const uint32_t* __restrict__ win, uint32_t* otypes,
+                                                              uint32_t* owin, uint64_t* ocounts,
+                                                              unsigned long long* state, uint32_t* slot,
+                                                              uint32_t* host_k) {
+  lookback_compact(
+      n,
+      [&](uint64_t i) {
+        const uint64_t x = counts[i];
+        return x != kPrunedDev && x >= threshold;
+      },
+      [&](uint64_t i, uint64_t o) {
+        for (uint32_t k = 0; k < L; ++k) otypes[o * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) owin[o * (L - 1) + k] = win[i * (L - 1) + k];
+        ocounts[o] = counts[i];
+      },
+      state, slot, host_k);
+}
+
+__global__ void __launch_bounds__(kLbThreads) prune_gather_lb(const unsigned long long* __restrict__ bound,
+                                                              uint64_t threshold, uint64_t n, uint32_t L,
+                                                              const uint32_t* __restrict__ types,
+                                                              const uint32_t* __restrict__ win,
+                                                              const uint32_t* __restrict__ sigma,
+                                                              uint64_t* counts, uint32_t* stypes, uint32_t* swin,
+                                                              uint32_t* ssigma, uint32_t* sidx,
+                                                              unsigned long long* state, uint32_t* slot,
+                                                              unsigned long long* pruned) {
+  uint32_t np = 0;
+  lookback_compact(
+      n,
+      [&](uint64_t i) {
+        const bool keep = bound[i] >= threshold;
+        counts[i] = keep ? 0 : kPrunedDev;
+        np += keep ? 0u : 1u;
+        return keep;
+      },
+      [&](uint64_t i, uint64_t o) {
+        for (uint32_t k = 0; k < L; ++k) stypes[o * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) swin[o * (L - 1) + k] = win[i * (L - 1) + k];
+        ssigma[o] = sigma[i];
+        sidx[o] = static_cast<uint32_t>(i);
+      },
+      state, slot, nullptr);
+  if (np) atomicAdd(pruned, static_cast<unsigned long long>(np));
 }
 
 // count >= threshold (never the PRUNED sentinel) -> compacted frequent set
@@ -794,21 +910,15 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   uint32_t* swin = reinterpret_cast<uint32_t*>(sbuf + s_win);
   uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
   uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
-  if (n <= kOneBlkMax) {
-    prune_gather_1blk<<<1, kOneBlk, 0, st_>>>(bound, threshold, n, L, c.types, c.win, c.sigma, d_counts,
-                                              stypes, swin, ssigma, sidx_out, slot_ptr(mslot), d_acc_ + 2);
+  {
+    const uint64_t nt = lb_tiles(n);
+    unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
+    EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
+    prune_gather_lb<<<static_cast<unsigned>(std::max<uint64_t>(nt, 1)), kLbThreads, 0, st_>>>(
+        bound, threshold, n, L, c.types, c.win, c.sigma, d_counts, stypes, swin, ssigma, sidx_out, lb,
+        slot_ptr(mslot), d_acc_ + 2);
     EPI_CUDA(cudaGetLastError());
     stats.kernel_launches += 3;
-  } else {
-    uint32_t* sflags = scratch_.get<uint32_t>(kMFlags, n);
-    uint32_t* sscan = scratch_.get<uint32_t>(kMScan, n);
-    prune_bound_kernel<<<blocks_for(n), 256, 0, st_>>>(bound, threshold, n, d_counts, sflags, d_acc_ + 2);
-    EPI_CUDA(cudaGetLastError());
-    dev_scan_total(sflags, sscan, n, mslot);
-    gather_kernel<<<blocks_for(n), 256, 0, st_>>>(sflags, sscan, n, L, c.types, c.win, c.sigma, stypes,
-                                                  swin, ssigma, sidx_out);
-    EPI_CUDA(cudaGetLastError());
-    stats.kernel_launches += 6;
   }
   DevSet sv = c;
   sv.types = stypes;
@@ -1109,6 +1219,16 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
                                                 reinterpret_cast<uint32_t*>(dm + o_t),
                                                 reinterpret_cast<uint32_t*>(dm + o_w),
                                                 reinterpret_cast<uint64_t*>(dm + o_c), slot_ptr(new_slot()), h_k);
+      EPI_CUDA(cudaGetLastError());
+      totals.kernel_launches += 1;
+    } else if (!std::getenv("EPI_COMPACT_CUB")) {
+      const uint64_t nt = lb_tiles(n);
+      unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
+      EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
+      compact_freq_lb<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
+          d_counts, cfg.threshold, n, L, d_types, d_win, reinterpret_cast<uint32_t*>(dm + o_t),
+          reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c), lb,
+          slot_ptr(new_slot()), h_k);
       EPI_CUDA(cudaGetLastError());
       totals.kernel_launches += 1;
     } else {
