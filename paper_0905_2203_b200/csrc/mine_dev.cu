@@ -475,10 +475,16 @@ constexpr int kBoundRound = kBoundPerWarp * (kBoundThreads / 32);
 template <int kF>
 __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch p) {
   __shared__ uint32_t D[16][kBoundThreads];
-  __shared__ uint32_t s_tau[kBoundRound], s_widx[kBoundRound];
-  __shared__ uint32_t s_acc[kBoundThreads / 32][kBoundPerWarp][32];
-  for (uint32_t x = threadIdx.x; x < (kBoundThreads / 32) * kBoundPerWarp * 32; x += kBoundThreads)
-    (&s_acc[0][0][0])[x] = 0;
+  // per round: the candidates' last type row offset and D row offset, the
+  // runs of equal last type (the join emits a left's candidates grouped so),
+  // and per-candidate per-lane partial sums
+  __shared__ uint32_t s_row[kBoundRound], s_drow[kBoundRound];
+  __shared__ uint32_t s_run[kBoundRound + 1];
+  __shared__ uint32_t s_nrun;
+  __shared__ uint32_t s_acc[kBoundRound][32];
+  __shared__ uint32_t s_x[kBoundThreads];               // phase A neighbour exchange
+  __shared__ uint32_t s_carry[kF > 0 ? kF : 1];         // U_k at the tile before the chunk
+  for (uint32_t x = threadIdx.x; x < kBoundRound * 32; x += kBoundThreads) (&s_acc[0][0])[x] = 0;
   const uint32_t l = blockIdx.x;
   const uint64_t c0 = max(p.loff ? p.loff[l] : l * p.stride, p.slice_lo);
   const uint64_t c1 = min(p.loff ? p.loff[l + 1] : (l + 1) * p.stride, p.slice_hi);
@@ -492,24 +498,93 @@ __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch 
   for (uint32_t r0 = 0; r0 < m; r0 += kBoundRound) {
     const uint32_t mr = min(m - r0, static_cast<uint32_t>(kBoundRound));
     __syncthreads();  // previous round's table reads are done
+    uint32_t my_tau = ~0u;
     for (uint32_t j = tid; j < mr; j += kBoundThreads) {
       const uint64_t cc = c0 + r0 + j;
-      s_tau[j] = p.ctypes[cc * p.L + p.L - 1];
+      my_tau = p.ctypes[cc * p.L + p.L - 1];
       const uint32_t w = p.cwin[cc * (p.L - 1) + p.L - 2];
       uint32_t x = 0;
       for (uint32_t a = 0; a < p.aw.n; ++a)
         if (p.aw.w[a] == w) x = a;
-      s_widx[j] = x;
+      s_row[j] = my_tau * kRowStride;
+      s_drow[j] = x * kBoundThreads;
     }
-    // this warp's candidates: j = warp + kWarps * i, i < nmine (<= 16);
-    // lane i keeps candidate i's running total
-    const uint32_t nmine = mr > warp ? (mr - warp + kWarps - 1) / kWarps : 0;
-    uint32_t acc = 0;
+    __syncthreads();
+    if (warp == 0) {
+      // run starts: j == 0 or a different last type than j - 1 (ballots over
+      // the round's <= kBoundRound candidates, in order)
+      uint32_t nrun = 0;
+      for (uint32_t j0 = 0; j0 < mr; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const bool start = j < mr && (j == 0 || s_row[j] != s_row[j - 1]);
+        const uint32_t bal = __ballot_sync(0xffffffffu, start);
+        if (start) s_run[nrun + __popc(bal & ((1u << lane) - 1))] = j;
+        nrun += __popc(bal);
+      }
+      if (lane == 0) {
+        s_run[nrun] = mr;
+        s_nrun = nrun;
+      }
+    }
+    __syncthreads();
+    const uint32_t nrun = s_nrun;
     for (int32_t gc = g_lo; gc < g_hi; gc += kBoundThreads) {
       // Phase A: dil_w(U(left)) for tile g = gc + tid, every alphabet window w
-      {
+      if constexpr (kF > 0) {
+        // one chain level at a time: thread = tile, U_{k-1} of the previous
+        // tile from the neighbour thread (shared memory), thread 0's from
+        // the previous chunk (s_carry) or, at a split start, rebuilt
         const int32_t g = gc + static_cast<int32_t>(tid);
-        constexpr int kU = kF > 0 ? kF + 1 : kBoundMaxL;
+        const bool in = g < p.n_tiles;
+        const size_t wbase = static_cast<size_t>(g >> 5) * p.blk_words + (g & 31);
+        if (tid == 0 && gc == g_lo) {
+          // U_k at tile g_lo - 1, k < F: the triangle over tiles g_lo-F .. g_lo-1
+          uint32_t u[kF];
+          auto occ_at = [&](uint32_t t, int32_t gj) -> uint32_t {
+            return (gj >= 0 && gj < p.n_tiles) ? __ldg(p.occ + impl::occ_index(gj, t, p.blk_words)) : 0u;
+          };
+          const uint32_t t0 = p.ltypes[static_cast<size_t>(l) * F];
+#pragma unroll
+          for (int j = 0; j < kF; ++j) u[j] = occ_at(t0, g_lo - kF + j);
+          s_carry[0] = u[kF - 1];
+#pragma unroll
+          for (int k = 1; k < kF; ++k) {
+            const uint32_t tk = p.ltypes[static_cast<size_t>(l) * F + k];
+            const uint32_t wk = p.lwin[static_cast<size_t>(l) * (F - 1) + k - 1];
+#pragma unroll
+            for (int j = kF - 1; j >= k; --j)
+              u[j] = occ_at(tk, g_lo - kF + j) &
+                     (p.uniform_w ? window_of(smear64(u[j - 1], u[j], p.sm, p.n_sm), wk) : dil_rt(wk, u[j - 1], u[j]));
+            s_carry[k] = u[kF - 1];
+          }
+        }
+        uint32_t u = in ? __ldg(p.occ + wbase + p.ltypes[static_cast<size_t>(l) * F] * kRowStride) : 0u;
+#pragma unroll
+        for (int k = 1; k <= kF; ++k) {
+          s_x[tid] = u;
+          __syncthreads();
+          const uint32_t prev = tid ? s_x[tid - 1] : s_carry[k - 1];
+          __syncthreads();
+          if (tid == kBoundThreads - 1) s_carry[k - 1] = u;  // the next chunk's thread 0
+          if (k < kF) {
+            const uint32_t tk = p.ltypes[static_cast<size_t>(l) * F + k];
+            const uint32_t wk = p.lwin[static_cast<size_t>(l) * (F - 1) + k - 1];
+            const uint32_t o = in ? __ldg(p.occ + wbase + tk * kRowStride) : 0u;
+            u = o & (p.uniform_w ? window_of(smear64(prev, u, p.sm, p.n_sm), wk) : dil_rt(wk, prev, u));
+          } else {
+            // U(left) at tiles g-1 (prev) and g (u); zero past the split
+            const bool live = g < g_hi;
+            if (p.uniform_w) {
+              const Smear64 sm = smear64(prev, u, p.sm, p.n_sm);
+              for (uint32_t a = 0; a < p.aw.n; ++a) D[a][tid] = live ? window_of(sm, p.aw.w[a]) : 0u;
+            } else {
+              for (uint32_t a = 0; a < p.aw.n; ++a) D[a][tid] = live ? dil_rt(p.aw.w[a], prev, u) : 0u;
+            }
+          }
+        }
+      } else {
+        const int32_t g = gc + static_cast<int32_t>(tid);
+        constexpr int kU = kBoundMaxL;
         uint32_t u[kU];  // u[j] = U at tile g - F + j, j = 0..F
         const uint32_t t0 = p.ltypes[static_cast<size_t>(l) * F];
         // word of type t at tile g - F + j (zero outside the stream)
@@ -552,33 +627,38 @@ __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch 
       const uint32_t q = lane >> 3, sub = (lane & 7) * 4;
       const uint32_t* blk0 = p.occ + static_cast<size_t>((gc >> 5) + q) * bw + sub;
       const uint32_t* dbase = &D[0][q * 32 + sub];
-      for (uint32_t i = 0; i < nmine; ++i) {
-        const uint32_t j = warp + kWarps * i;
-        const uint4* row = reinterpret_cast<const uint4*>(blk0 + s_tau[j] * kRowStride);
-        const uint32_t* drow = dbase + s_widx[j] * kBoundThreads;
-        uint32_t a = 0;
+      // a warp takes a run: its last type's rows are loaded once, then every
+      // candidate of the run (one per alphabet window) ANDs and counts them
+      for (uint32_t r = warp; r < nrun; r += kWarps) {
+        const uint32_t j0 = s_run[r], j1 = s_run[r + 1];
+        const uint32_t* row = blk0 + s_row[j0];
+        uint4 o[kBoundThreads / 128];
 #pragma unroll
-        for (int m = 0; m < kBoundThreads / 128; ++m) {
-          if (static_cast<int32_t>(q) + 4 * m < nk) {
-            const uint4 o = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(row) + 4 * m * bw));
+        for (int m = 0; m < kBoundThreads / 128; ++m)
+          o[m] = static_cast<int32_t>(q) + 4 * m < nk
+                     ? __ldg(reinterpret_cast<const uint4*>(row + 4 * m * bw))
+                     : make_uint4(0, 0, 0, 0);
+        for (uint32_t j = j0; j < j1; ++j) {
+          const uint32_t* drow = dbase + s_drow[j];
+          uint32_t a = 0;
+#pragma unroll
+          for (int m = 0; m < kBoundThreads / 128; ++m) {
             const uint4 d = *reinterpret_cast<const uint4*>(drow + 128 * m);
-            a += __popc(o.x & d.x) + __popc(o.y & d.y) + __popc(o.z & d.z) + __popc(o.w & d.w);
+            a += __popc(o[m].x & d.x) + __popc(o[m].y & d.y) + __popc(o[m].z & d.z) + __popc(o[m].w & d.w);
           }
+          s_acc[j][lane] += a;
         }
-        s_acc[warp][i][lane] += a;
       }
       __syncthreads();
     }
-    // per candidate: sum the 32 lanes' partials
-    for (uint32_t i = 0; i < nmine; ++i) {
-      uint32_t v = s_acc[warp][i][lane];
-      s_acc[warp][i][lane] = 0;
+    // per candidate: sum the 32 lanes' partials (warp per candidate)
+    for (uint32_t j = warp; j < mr; j += kWarps) {
+      uint32_t v = s_acc[j][lane];
+      s_acc[j][lane] = 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == i) acc = v;
+      if (lane == 0 && v) atomicAdd(p.bound + (c0 - p.slice_lo) + r0 + j, static_cast<unsigned long long>(v));
     }
-    if (lane < nmine && acc)
-      atomicAdd(p.bound + (c0 - p.slice_lo) + r0 + warp + kWarps * lane, static_cast<unsigned long long>(acc));
   }
 }
 
