@@ -94,22 +94,6 @@ void launch_walk(int n_nodes, const CountLaunch& p, cudaStream_t st) {
   NarrowAll::walk(n_nodes, p, st);
 }
 
-namespace {
-// out += sum over the episode-type slots of the events of that type.
-__global__ void matched_pairs_kernel(const uint32_t* __restrict__ types, uint64_t count,
-                                     const uint32_t* __restrict__ n_dev, uint32_t per,
-                                     const unsigned long long* __restrict__ hist,
-                                     unsigned long long* out) {
-  if (n_dev) count = static_cast<uint64_t>(*n_dev) * per;
-  unsigned long long acc = 0;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    acc += hist[types[i]];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
-}
-}  // namespace
 
 namespace {
 // Single-node episodes: every distinct firing time of the type is one
@@ -143,14 +127,5 @@ void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_block
   EPI_CUDA(cudaGetLastError());
 }
 
-void launch_matched_pairs(const uint32_t* types, uint64_t count, const uint32_t* n_dev, uint32_t per,
-                          const unsigned long long* hist, unsigned long long* out, cudaStream_t st) {
-  if (count == 0 || hist == nullptr) return;
-  uint64_t blocks = (count + 255) / 256;
-  if (blocks > 1184) blocks = 1184;
-  matched_pairs_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(types, count, n_dev, per, hist,
-                                                                      out);
-  EPI_CUDA(cudaGetLastError());
-}
 
 }  // namespace epi

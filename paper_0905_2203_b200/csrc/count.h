@@ -37,6 +37,8 @@ struct CountLaunch {
   int* occ_query;            // host: non-null -> launch_machines* reports CTAs/SM, no launch
   uint32_t last_sh[4];       // launch_machines_last: doubling-smear shifts of the last window
   int32_t walk_warp;         // concat walk: one warp per episode (walk_warp_kernel, P <= 128)
+  const unsigned long long* hist;  // events per type (matched-pair statistics), may be null
+  unsigned long long* matched;     // += sum over live episodes of sum_k hist[type_k]
 };
 
 // Doubling-smear shift amounts covering a window of width w (1..16).
@@ -66,9 +68,6 @@ void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 // Exact counts of single-node episodes (popcount of the type's bitmap).
 void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_blocks,
                        const uint32_t* types, uint32_t n_eps, uint64_t* counts, cudaStream_t st);
-// *out += sum_i hist[types[i]] over i < count (or < *n_dev * per when
-// n_dev is set): the matched-pair work model of a launch.
-void launch_matched_pairs(const uint32_t* types, uint64_t count, const uint32_t* n_dev, uint32_t per,
-                          const unsigned long long* hist, unsigned long long* out, cudaStream_t st);
+
 
 }  // namespace epi

@@ -428,6 +428,18 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   const int32_t g0 = (gq - p.window_tiles > 0 ? gq - p.window_tiles : 0) & ~3;
 
   EpParams<N> ep = load_episode<N>(p, active ? e : 0);
+  if (q == 0 && p.matched) {
+    // matched-pair work of the launch (statistics): the first segment's
+    // CTAs add their episodes' sum_k events(type_k)
+    unsigned long long mp = 0;
+    if (active) {
+#pragma unroll
+      for (int k = 0; k < N; ++k) mp += p.hist[ep.type[k]];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mp += __shfl_xor_sync(0xffffffffu, mp, o);
+    if ((threadIdx.x & 31) == 0 && mp) atomicAdd(p.matched, mp);
+  }
   Machine<N, Hist> m;
   m.hist.reset(g0, p.hist_words);
   const int64_t tq = static_cast<int64_t>(gq) * 32;

@@ -425,8 +425,10 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // bitmap is zero past the stream).
   const int64_t seg_len = ((tiles4 + P - 1) / P + 3) / 4 * 4;
   P = (tiles4 + seg_len - 1) / seg_len;
-  // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k).
-  launch_matched_pairs(ds.types, n * N, n_dev, N, stream_.d_hist, d_acc_ + 1, st_);
+  // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k),
+  // accumulated by the map kernel's first segment.
+  p.hist = stream_.d_hist;
+  p.matched = d_acc_ + 1;
 
   const size_t nm = P > 1 ? static_cast<size_t>(P) * n : 1;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
@@ -463,7 +465,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   }
   timed_.push_back(t);
   stats.segments = static_cast<uint64_t>(P);
-  stats.kernel_launches += P > 1 ? 3 : 2;  // matched-pair stats + map (+ walk)
+  stats.kernel_launches += P > 1 ? 2 : 1;  // map (+ walk)
   stats.map_launches += 1;
 }
 

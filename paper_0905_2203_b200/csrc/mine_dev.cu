@@ -267,28 +267,43 @@ __device__ __forceinline__ void lookback_compact(uint64_t n, Pred&& pred, Emit&&
     if (b + j < n && pred(b + j)) bits |= 1u << j;
   uint32_t off = 0, agg = 0;
   BS(ts).ExclusiveSum(static_cast<uint32_t>(__popc(bits)), off, agg);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0: publish the aggregate, then look back 32 predecessors at a time
+    const uint32_t lane = threadIdx.x;
     cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(state[1 + tile]);
     unsigned long long excl = 0;
     if (tile == 0) {
-      me.store(kLbIncl | agg, cuda::memory_order_release);
+      if (lane == 0) me.store(kLbIncl | agg, cuda::memory_order_release);
     } else {
-      me.store(kLbAgg | agg, cuda::memory_order_release);
-      for (uint32_t t = tile; t-- > 0;) {
-        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(state[1 + t]);
-        unsigned long long v;
-        while (((v = st.load(cuda::memory_order_acquire)) >> 62) == 0) {
+      if (lane == 0) me.store(kLbAgg | agg, cuda::memory_order_release);
+      int64_t top = static_cast<int64_t>(tile) - 1;  // newest predecessor not yet summed
+      while (true) {
+        const int64_t t = top - lane;  // lane 0 = nearest
+        unsigned long long v = kLbIncl;  // before tile 0: an empty inclusive prefix
+        if (t >= 0) {
+          cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(state[1 + t]);
+          while (((v = st.load(cuda::memory_order_acquire)) >> 62) == 0) {
+          }
         }
-        excl += v & kLbVal;
-        if ((v >> 62) == 2) break;
+        const uint32_t incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        // sum lanes up to and including the nearest inclusive prefix
+        const uint32_t stop = incl ? __ffs(incl) - 1 : 31;
+        unsigned long long x = (lane <= stop && t >= 0) ? (v & kLbVal) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        excl += x;
+        if (incl) break;
+        top -= 32;
       }
-      me.store(kLbIncl | (excl + agg), cuda::memory_order_release);
+      if (lane == 0) me.store(kLbIncl | (excl + agg), cuda::memory_order_release);
     }
-    s_excl = excl;
-    if (base + kLbTile >= n) {  // the last tile knows the total
-      const uint32_t total = static_cast<uint32_t>(excl + agg);
-      *total_slot = total;
-      if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
+    if (lane == 0) {
+      s_excl = excl;
+      if (base + kLbTile >= n) {  // the last tile knows the total
+        const uint32_t total = static_cast<uint32_t>(excl + agg);
+        *total_slot = total;
+        if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
+      }
     }
   }
   __syncthreads();
