@@ -392,3 +392,26 @@ def test_mine_pass1_every_level_vs_reference(ctx, seed, pass1, monkeypatch):
     r = mine(s, MiningConfig(threshold=thr, constraint_alphabet=bins, max_level=5, mode=MODE_MINE), ctx=ctx)
     assert [lv.candidates for lv in r.levels] == cands_ref, seed
     assert write_mining_csv(r) == csv_ref, seed
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_mine_wide_windows_vs_reference(ctx, seed, monkeypatch):
+    """Constraint alphabets with high > 32 (popcount pass 1 off; the
+    last-constraint hull pass 1 forced on every level; wide-window map
+    kernels for high > 63): mining CSV == the reference's mine()."""
+    from paper_0905_2203_b200 import EventStream, MiningConfig, mine, write_mining_csv
+    monkeypatch.setenv("EPI_PASS1_MIN", "1")
+    rng = np.random.default_rng(5100 + seed)
+    a = int(rng.integers(3, 6))
+    n = int(rng.integers(1500, 3000))
+    times = np.cumsum(rng.integers(0, [20, 40, 10][seed] + 1, n)).astype(np.int64)
+    types = rng.integers(0, a, n).astype(np.uint32)
+    bins = [[(0, 40), (40, 80)], [(10, 50), (0, 120)], [(0, 33), (33, 66), (66, 99)]][seed]
+    thr = int(max(2, n // (a * a * 2)))
+    csv_ref, cands_ref, _ = oracle.ref_mine(types, times, a, thr, bins, 4, switch_level=99, backend=0,
+                                            workers=4)
+    s = EventStream(types, times, a)
+    for mode in (MODE_MINE, MODE_EXACT):
+        r = mine(s, MiningConfig(threshold=thr, constraint_alphabet=bins, max_level=4, mode=mode), ctx=ctx)
+        assert [lv.candidates for lv in r.levels] == cands_ref, (seed, mode)
+        assert write_mining_csv(r) == csv_ref, (seed, mode)
