@@ -199,9 +199,15 @@ def test_cfg1_all_pairs(ctx, golden_configs):
     assert fnv_u64s(got) == g["fnv_counts"]
 
 
-@pytest.mark.parametrize("mode", [MODE_MINE, MODE_EXACT])
-def test_cfg2_mining(ctx, golden_configs, mode):
+@pytest.mark.parametrize("mode,knob", [(MODE_MINE, None), (MODE_EXACT, None), (MODE_MINE, "EPI_COMPACT_CUB"),
+                                       (MODE_MINE, "EPI_PASS1_HULL"), (MODE_MINE, "EPI_WALK_SEQ")])
+def test_cfg2_mining(ctx, golden_configs, mode, knob, monkeypatch):
+    """cfg2 mining CSV == the reference's, on the default device path and on
+    each alternative it keeps (CUB multi-kernel compaction, hull pass 1,
+    sequential concat walk)."""
     from paper_0905_2203_b200 import MiningConfig, mine, write_mining_csv, EventStream
+    if knob:
+        monkeypatch.setenv(knob, "1")
     g = golden_configs["cfg2"]
     types, times = generate_arrays(_gen("cfg2"))
     s = EventStream(types, times, 26)
