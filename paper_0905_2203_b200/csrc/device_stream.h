@@ -31,9 +31,11 @@ class DeviceScratch {
       size_t grow = bytes + bytes / 4;
       EPI_CUDA(cudaMalloc(&b.p, grow));
       b.bytes = grow;
+      ++generation;
     }
     return static_cast<T*>(b.p);
   }
+  uint64_t generation = 0;  // bumped on every reallocation (graph-cache validity)
 
  private:
   struct Buf {
@@ -50,6 +52,7 @@ struct DeviceStream {
   uint64_t n_tiles = 0;    // 32 ms tiles covering the compressed span
   uint64_t span = 0;       // compressed time span (last compressed time + 1)
   uint32_t gap_cap = 64;   // gap compression cap of the current bitmap (> every high)
+  uint64_t generation = 0;    // bumped when d_occ is reallocated
   uint32_t* d_occ = nullptr;  // blocked bitmaps, see count.h (kBlkTiles, kRowStride)
   uint32_t blk_words = 0;     // words per bitmap block (a_pad * kRowStride)
   size_t occ_bytes = 0;

@@ -84,6 +84,8 @@ Engine::Engine(int device) : device_(device) {
 
 Engine::~Engine() {
   cudaSetDevice(device_);
+  for (auto& kv : level_graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   stream_.release();
   if (ev0_) cudaEventDestroy(ev0_);
   if (ev1_) cudaEventDestroy(ev1_);
@@ -95,6 +97,16 @@ Engine::~Engine() {
 }
 
 // ---- deferred statistics -----------------------------------------------------
+
+void Engine::rec(cudaEvent_t e) {
+  EPI_CUDA(cudaEventRecordWithFlags(e, st_, capturing_ ? cudaEventRecordExternal : cudaEventRecordDefault));
+}
+
+uint64_t Engine::buffers_generation() const {
+  return scratch_.generation * 0x9e3779b97f4a7c15ull ^ (stream_.generation << 1) ^
+         (pin_up_.generation << 9) ^ (pin_small_.generation << 17) ^ (map_out_.generation << 25) ^
+         (map_small_.generation << 33);
+}
 
 void Engine::begin_op() {
   ++stat_epoch_;
@@ -309,10 +321,10 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     Timed t{next_event(), nullptr, next_event(), ms_out, -1, n,
             static_cast<uint64_t>(n_blocks) * kBlkTiles, true};
     t.e_map = t.e1;
-    EPI_CUDA(cudaEventRecord(t.e0, st_));
+    rec(t.e0);
     launch_singletons(stream_.d_occ, stream_.blk_words, n_blocks, ds.types, static_cast<uint32_t>(n),
                       d_counts, st_);
-    EPI_CUDA(cudaEventRecord(t.e1, st_));
+    rec(t.e1);
     timed_.push_back(t);
     stats.kernel_launches += 1;
     stats.map_launches += 1;
@@ -451,9 +463,9 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     tiles += static_cast<uint64_t>(gn - std::max<int64_t>(gq - window_tiles, 0));
   }
   Timed t{next_event(), next_event(), nullptr, ms_out, live_slot, n, tiles, true};
-  EPI_CUDA(cudaEventRecord(t.e0, st_));
+  rec(t.e0);
   launch_map();
-  EPI_CUDA(cudaEventRecord(t.e_map, st_));
+  rec(t.e_map);
   t.e1 = t.e_map;
   if (P > 1) {
     if (wide)
@@ -461,7 +473,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     else
       launch_walk(static_cast<int>(N), p, st_);
     t.e1 = next_event();
-    EPI_CUDA(cudaEventRecord(t.e1, st_));
+    rec(t.e1);
   }
   timed_.push_back(t);
   stats.segments = static_cast<uint64_t>(P);

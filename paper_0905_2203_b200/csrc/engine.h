@@ -59,8 +59,10 @@ struct MappedBuffer {
       EPI_CUDA(cudaHostAlloc(&p, grow, cudaHostAllocMapped));
       EPI_CUDA(cudaHostGetDevicePointer(&d, p, 0));
       bytes = grow;
+      ++generation;
     }
   }
+  uint64_t generation = 0;
 };
 
 struct PinnedBuffer {
@@ -76,9 +78,11 @@ struct PinnedBuffer {
       size_t grow = need + need / 4 + 4096;
       EPI_CUDA(cudaMallocHost(&p, grow));
       bytes = grow;
+      ++generation;
     }
     return p;
   }
+  uint64_t generation = 0;
 };
 
 class Engine {
@@ -152,6 +156,7 @@ class Engine {
   // nothing was launched in between.
   void prefetch_stats();
   uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
+
   cudaEvent_t next_event();
   int new_slot();  // a device u32 log slot, unique within the call
   uint32_t* slot_ptr(int s) { return d_log_ + s; }
@@ -171,6 +176,34 @@ class Engine {
   std::vector<cudaEvent_t> ev_pool_;
   size_t ev_used_ = 0;
   std::vector<Timed> timed_;
+  // ---- per-level CUDA graphs (epi_mine) -----------------------------------
+  // A mining level's device work (upload, generation, passes, compaction,
+  // statistics prefetch) depends on the host only through the values in its
+  // key; the second time a key is seen the enqueue is captured into a graph,
+  // from then on the graph is relaunched and the enqueue's host-side
+  // bookkeeping replayed. The key includes every buffer generation, so a
+  // reallocation invalidates it.
+  struct LevelGraph {
+    cudaGraphExec_t exec = nullptr;
+    bool capturable = true;
+    int seen = 0;
+    epi_stats delta{};
+    uint64_t segments_after = 0;
+    bool segments_set = false;
+    std::vector<Timed> timed;            // ms pointers stored as offsets into epi_stats
+    std::vector<SlotCounter> slots;      // targets stored as offsets into epi_stats
+    int log_start = 0, log_end = 0;
+    size_t ev_start = 0, ev_end = 0;
+  };
+  std::vector<std::pair<std::string, LevelGraph>> level_graphs_;
+  bool capturing_ = false;
+  void rec(cudaEvent_t e);  // event record, external node while capturing
+  uint64_t buffers_generation() const;
+  // Runs `enqueue` (the level's device work) directly, captured, or as a
+  // replayed graph; `stats` is the call's accumulator.
+  template <class F>
+  void run_level(const std::string& key, bool graphable, epi_stats& stats, F&& enqueue);
+
   std::vector<SlotCounter> slot_counters_;
   uint32_t* d_log_ = nullptr;            // kLogSlots u32
   unsigned long long* d_acc_ = nullptr;  // [0] patches [1] matched pairs [2] pruned

@@ -262,6 +262,7 @@ void DeviceStream::ensure_occ(uint64_t tiles, cudaStream_t st) {
     d_occ = nullptr;
     occ_bytes = 0;
     EPI_CUDA(cudaMalloc(&d_occ, need));
+    ++generation;
     occ_bytes = need;
   }
   EPI_CUDA(cudaMemsetAsync(d_occ, 0, need, st));

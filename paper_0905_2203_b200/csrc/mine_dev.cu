@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstddef>
 #include <cstdio>
+#include <string>
 #include <cstdlib>
 #include <numeric>
 
@@ -980,7 +982,7 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   t.e_map = t.e1;
   t.ms_out2 = &stats.bound_ms;
   stats.bound_words += n * static_cast<uint64_t>(stream_.n_tiles);
-  EPI_CUDA(cudaEventRecord(t.e0, st_));
+  rec(t.e0);
   const dim3 grid(static_cast<unsigned>(lf.nf), static_cast<unsigned>(std::max<int64_t>(ysplits, 1)));
   switch (L - 1) {
     case 1: bound_kernel<1><<<grid, kBoundThreads, 0, st_>>>(b); break;
@@ -992,7 +994,7 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
     default: bound_kernel<0><<<grid, kBoundThreads, 0, st_>>>(b); break;
   }
   EPI_CUDA(cudaGetLastError());
-  EPI_CUDA(cudaEventRecord(t.e1, st_));
+  rec(t.e1);
   timed_.push_back(t);
 
   const int mslot = new_slot();
@@ -1024,6 +1026,130 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   scatter_counts_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx_out, sc, slot_ptr(mslot), d_counts);
   EPI_CUDA(cudaGetLastError());
   stats.kernel_launches += 2;
+}
+
+// ---- per-level CUDA graphs ---------------------------------------------------
+
+namespace {
+// epi_stats as counters (u64 fields, then doubles), for deltas
+constexpr size_t kStatU64 = offsetof(epi_stats, pass1_ms) / sizeof(uint64_t);
+void stats_axpy(epi_stats& a, const epi_stats& b, int sign) {
+  auto* au = reinterpret_cast<uint64_t*>(&a);
+  const auto* bu = reinterpret_cast<const uint64_t*>(&b);
+  for (size_t i = 0; i < kStatU64; ++i) au[i] += sign > 0 ? bu[i] : (0 - bu[i]);
+  double* ad[] = {&a.pass1_ms, &a.pass2_ms, &a.map_ms, &a.concat_ms, &a.total_ms, &a.bound_ms};
+  const double bd[] = {b.pass1_ms, b.pass2_ms, b.map_ms, b.concat_ms, b.total_ms, b.bound_ms};
+  for (int i = 0; i < 6; ++i) *ad[i] += sign * bd[i];
+  a.bound_words += sign > 0 ? b.bound_words : (0 - b.bound_words);
+}
+}  // namespace
+
+template <class F>
+void Engine::run_level(const std::string& key, bool graphable, epi_stats& stats, F&& enqueue) {
+  if (!graphable || std::getenv("EPI_NO_GRAPH")) {
+    enqueue();
+    return;
+  }
+  LevelGraph* g = nullptr;
+  for (auto& kv : level_graphs_)
+    if (kv.first == key) g = &kv.second;
+  if (!g) {
+    if (level_graphs_.size() >= 64) {  // bounded cache
+      for (auto& kv : level_graphs_)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      level_graphs_.clear();
+    }
+    level_graphs_.emplace_back(key, LevelGraph{});
+    g = &level_graphs_.back().second;
+  }
+  char* const base = reinterpret_cast<char*>(&stats);
+  auto off_of = [&](const void* ptr) -> ptrdiff_t {
+    if (!ptr) return -1;
+    const ptrdiff_t o = static_cast<const char*>(ptr) - base;
+    return o >= 0 && o < static_cast<ptrdiff_t>(sizeof(epi_stats)) ? o : -2;
+  };
+  if (g->exec && g->log_start == log_used_ && g->ev_start == ev_used_) {
+    // replay: relaunch the graph, then its enqueue's host bookkeeping
+    EPI_CUDA(cudaGraphLaunch(g->exec, st_));
+    stats_axpy(stats, g->delta, +1);
+    if (g->segments_set) stats.segments = g->segments_after;
+    for (const Timed& t : g->timed) {
+      Timed r = t;
+      r.ms_out = t.ms_out ? reinterpret_cast<double*>(base + reinterpret_cast<ptrdiff_t>(t.ms_out)) : nullptr;
+      r.ms_out2 = t.ms_out2 ? reinterpret_cast<double*>(base + reinterpret_cast<ptrdiff_t>(t.ms_out2)) : nullptr;
+      timed_.push_back(r);
+    }
+    for (const SlotCounter& sc : g->slots)
+      slot_counters_.push_back({sc.slot, reinterpret_cast<uint64_t*>(base + reinterpret_cast<ptrdiff_t>(sc.target))});
+    log_used_ = g->log_end;
+    ev_used_ = g->ev_end;
+    ++stat_epoch_;
+    prefetched_epoch_ = stat_epoch_;  // the graph ends with the statistics prefetch
+    return;
+  }
+  if (!g->capturable || g->exec || g->seen == 0) {
+    // first sighting (warms every buffer the level needs) or a slot/event
+    // position the graph was not captured at: run directly
+    ++g->seen;
+    enqueue();
+    return;
+  }
+  // capture the enqueue, launch it, remember its bookkeeping
+  const epi_stats before = stats;
+  const size_t t0 = timed_.size(), s0 = slot_counters_.size();
+  const int log0 = log_used_;
+  const size_t ev0 = ev_used_;
+  const uint64_t gen0 = buffers_generation();
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool ok = cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    capturing_ = true;
+    try {
+      enqueue();
+    } catch (...) {
+      ok = false;
+    }
+    capturing_ = false;
+    if (cudaStreamEndCapture(st_, &graph) != cudaSuccess || !graph) ok = false;
+  }
+  if (ok && buffers_generation() != gen0) ok = false;
+  if (ok && cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) ok = false;
+  if (graph) cudaGraphDestroy(graph);
+  for (size_t i = t0; ok && i < timed_.size(); ++i)
+    if (off_of(timed_[i].ms_out) == -2 || off_of(timed_[i].ms_out2) == -2) ok = false;
+  for (size_t i = s0; ok && i < slot_counters_.size(); ++i)
+    if (off_of(slot_counters_[i].target) < 0) ok = false;
+  if (!ok) {
+    cudaGetLastError();
+    if (exec) cudaGraphExecDestroy(exec);
+    stats = before;
+    timed_.resize(t0);
+    slot_counters_.resize(s0);
+    log_used_ = log0;
+    ev_used_ = ev0;
+    g->capturable = false;
+    enqueue();
+    return;
+  }
+  EPI_CUDA(cudaGraphLaunch(exec, st_));
+  g->exec = exec;
+  g->delta = stats;
+  stats_axpy(g->delta, before, -1);
+  g->segments_set = stats.segments != before.segments;
+  g->segments_after = stats.segments;
+  g->delta.segments = 0;
+  g->timed.assign(timed_.begin() + static_cast<ptrdiff_t>(t0), timed_.end());
+  for (Timed& t : g->timed) {
+    t.ms_out = t.ms_out ? reinterpret_cast<double*>(off_of(t.ms_out)) : nullptr;
+    t.ms_out2 = t.ms_out2 ? reinterpret_cast<double*>(off_of(t.ms_out2)) : nullptr;
+  }
+  g->slots.assign(slot_counters_.begin() + static_cast<ptrdiff_t>(s0), slot_counters_.end());
+  for (SlotCounter& sc : g->slots) sc.target = reinterpret_cast<uint64_t*>(off_of(sc.target));
+  g->log_start = log0;
+  g->log_end = log_used_;
+  g->ev_start = ev0;
+  g->ev_end = ev_used_;
 }
 
 // mine (E/miner.hpp:114-173), device-resident; with `shard`, each large
@@ -1212,60 +1338,52 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     PopLefts lefts;  // the join's lefts on the device (popcount pass 1)
     lefts.nf = nf;
     lefts.slice_lo = lo_c;
+    // ---- host prep: the level's upload into pinned memory ------------------
+    size_t up_bytes = 0;
+    char* h_up = nullptr;
+    char* d_up = nullptr;
+    size_t o_s = 0, o_p = 0, o_r = 0, o_o = 0;  // join upload layout (level >= 3)
     if (level == 1) {
-      uint32_t* h = static_cast<uint32_t*>(pin_up_.get(n * 4));
-      std::iota(h, h + n, 0u);
-      EPI_CUDA(cudaMemcpyAsync(d_types, h, n * 4, cudaMemcpyHostToDevice, st_));
-      totals.h2d_bytes += n * 4;
+      up_bytes = n * 4;
+      h_up = static_cast<char*>(pin_up_.get(up_bytes));
+      std::iota(reinterpret_cast<uint32_t*>(h_up), reinterpret_cast<uint32_t*>(h_up) + n, 0u);
+      d_up = reinterpret_cast<char*>(d_types);
     } else if (level == 2) {
       const size_t up = nf + 2 * cfg.n_alpha;
-      uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up * 4));
+      up_bytes = up * 4;
+      uint32_t* h = static_cast<uint32_t*>(pin_up_.get(up_bytes));
       std::copy(ftypes.begin(), ftypes.end(), h);
       std::copy(awin.begin(), awin.end(), h + nf);
       std::copy(ahi.begin(), ahi.end(), h + nf + cfg.n_alpha);
-      uint32_t* d = scratch_.get<uint32_t>(kMFreq, up);
-      EPI_CUDA(cudaMemcpyAsync(d, h, up * 4, cudaMemcpyHostToDevice, st_));
-      totals.h2d_bytes += up * 4;
-      lefts.types = d;
+      h_up = reinterpret_cast<char*>(h);
+      d_up = reinterpret_cast<char*>(scratch_.get<uint32_t>(kMFreq, up));
+      lefts.types = reinterpret_cast<const uint32_t*>(d_up);
       lefts.stride = static_cast<uint64_t>(nf) * cfg.n_alpha;
-      gen_level2_kernel<<<blocks_for(n), 256, 0, st_>>>(d, static_cast<uint32_t>(nf), d + nf,
-                                                        d + nf + cfg.n_alpha,
-                                                        static_cast<uint32_t>(cfg.n_alpha), d_types,
-                                                        d_win, d_sigma, n);
-      EPI_CUDA(cudaGetLastError());
     } else {
-      // upload: frequent types/win/sigma + pre + lrange + loff
-      const size_t o_t = 0, o_w = align256(nf * F * 4), o_s = o_w + align256(nf * (F - 1) * 4),
-                   o_p = o_s + align256(nf * 4), o_r = o_p + align256(nf * 4),
-                   o_o = o_r + align256(nf * 8), o_end = o_o + align256((nf + 1) * 8);
-      char* h = static_cast<char*>(pin_up_.get(o_end));
-      std::memcpy(h + o_t, ftypes.data(), nf * F * 4);
-      std::memcpy(h + o_w, fwin.data(), nf * (F - 1) * 4);
-      uint32_t* hs = reinterpret_cast<uint32_t*>(h + o_s);
+      // frequent types/win/sigma + pre + lrange + loff
+      const size_t o_w = align256(nf * F * 4);
+      o_s = o_w + align256(nf * (F - 1) * 4);
+      o_p = o_s + align256(nf * 4);
+      o_r = o_p + align256(nf * 4);
+      o_o = o_r + align256(nf * 8);
+      up_bytes = o_o + align256((nf + 1) * 8);
+      h_up = static_cast<char*>(pin_up_.get(up_bytes));
+      std::memcpy(h_up, ftypes.data(), nf * F * 4);
+      std::memcpy(h_up + o_w, fwin.data(), nf * (F - 1) * 4);
+      uint32_t* hs = reinterpret_cast<uint32_t*>(h_up + o_s);
       for (size_t i = 0; i < nf; ++i) {
         uint32_t sg = 0;
         for (uint32_t k = 0; k + 1 < F; ++k) sg += fwin[i * (F - 1) + k] >> 16;
         hs[i] = sg;
       }
-      std::memcpy(h + o_p, pre.data(), nf * 4);
-      std::memcpy(h + o_r, lrange.data(), nf * 8);
-      std::memcpy(h + o_o, loff.data(), (nf + 1) * 8);
-      char* d = scratch_.get<char>(kMJoin, o_end);
-      EPI_CUDA(cudaMemcpyAsync(d, h, o_end, cudaMemcpyHostToDevice, st_));
-      totals.h2d_bytes += o_end;
-      lefts.types = reinterpret_cast<const uint32_t*>(d + o_t);
-      lefts.win = reinterpret_cast<const uint32_t*>(d + o_w);
-      lefts.off = reinterpret_cast<const uint64_t*>(d + o_o);
-      const unsigned blocks = static_cast<unsigned>((nf * 32 + 255) / 256);
-      gen_join_kernel<<<blocks, 256, 0, st_>>>(
-          L, reinterpret_cast<const uint32_t*>(d + o_t), reinterpret_cast<const uint32_t*>(d + o_w),
-          reinterpret_cast<const uint32_t*>(d + o_s), static_cast<uint32_t>(nf),
-          reinterpret_cast<const uint32_t*>(d + o_p), reinterpret_cast<const uint32_t*>(d + o_r),
-          reinterpret_cast<const uint64_t*>(d + o_o), d_types, d_win, d_sigma);
-      EPI_CUDA(cudaGetLastError());
+      std::memcpy(h_up + o_p, pre.data(), nf * 4);
+      std::memcpy(h_up + o_r, lrange.data(), nf * 8);
+      std::memcpy(h_up + o_o, loff.data(), (nf + 1) * 8);
+      d_up = scratch_.get<char>(kMJoin, up_bytes);
+      lefts.types = reinterpret_cast<const uint32_t*>(d_up);
+      lefts.win = reinterpret_cast<const uint32_t*>(d_up + o_w);
+      lefts.off = reinterpret_cast<const uint64_t*>(d_up + o_o);
     }
-    if (level > 1) totals.kernel_launches += 1;
-
     DevSet c;
     c.N = L;
     c.n = cnt_c;
@@ -1275,80 +1393,138 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     c.max_high = amax;
     c.max_sigma = static_cast<uint32_t>(amax * (L - 1));
     c.width = awidth > 0 ? awidth : 0;
-    g_trace.mark("gen launched");
     // Pass 1 by the popcount bound when the level is large enough to pay
     // and every window fits one history word; else the hull relaxation.
     const bool popbound = cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 && n >= min_pass1() &&
                           amax <= 32 && cfg.n_alpha <= 16 && L <= static_cast<uint32_t>(kBoundMaxL) &&
                           !std::getenv("EPI_PASS1_HULL");
-    if (level == 1) {
-      // single-node episodes: a popcount of each type's bitmap row
-      totals.episodes += n;
-      totals.pass2_episodes += n;
-      count_device(c, d_counts, totals, &totals.pass2_ms);
-    } else if (cnt_c > 0 && popbound)
-      count_device_popbound(c, lefts, cfg.threshold, awin.data(), static_cast<uint32_t>(cfg.n_alpha),
-                            d_counts + lo_c, totals);
-    else if (cnt_c > 0)
-      count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, awin.data(),
-                            static_cast<uint32_t>(cfg.n_alpha), d_counts + lo_c, totals);
-    g_trace.mark("count launched");
-    if (sharded) {
-      // every rank's s-wide slice -> the full count vector in candidate order
-      uint64_t* d_all = scratch_.get<uint64_t>(kMGather, s * W);
-      const int rc = shard->allgather(shard->user, d_counts + static_cast<uint64_t>(R) * s, d_all,
-                                      s * sizeof(uint64_t), static_cast<void*>(st_));
-      if (rc != 0) throw Error(EPI_ENCCL, "mine: all-gather of level counts failed");
-      d_counts = d_all;
-    }
-
-    // ---- threshold + compaction in candidate order, straight to host -----
+    // the hull pass 1 synchronises mid-level (its group count): not graphable
+    const bool hull_pass1 = level > 1 && !popbound && cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 &&
+                            n >= min_pass1();
     map_small_.get(64);
     uint32_t* h_k = static_cast<uint32_t*>(map_small_.p) + 1;
-    const size_t o_t = 0, o_w = align256(static_cast<size_t>(n) * L * 4),
-                 o_c = o_w + align256(static_cast<size_t>(n) * (L - 1) * 4), o_end = o_c + align256(n * 8ull);
-    map_out_.get(o_end);
+    const size_t o_ft = 0, o_fw = align256(static_cast<size_t>(n) * L * 4),
+                 o_fc = o_fw + align256(static_cast<size_t>(n) * (L - 1) * 4), o_fend = o_fc + align256(n * 8ull);
+    map_out_.get(o_fend);
     char* dm = static_cast<char*>(map_out_.d);
-    if (n <= kOneBlkMax) {
-      compact_freq_1blk<<<1, kOneBlk, 0, st_>>>(d_counts, cfg.threshold, n, L, d_types, d_win,
-                                                reinterpret_cast<uint32_t*>(dm + o_t),
-                                                reinterpret_cast<uint32_t*>(dm + o_w),
-                                                reinterpret_cast<uint64_t*>(dm + o_c), slot_ptr(new_slot()), h_k);
-      EPI_CUDA(cudaGetLastError());
-      totals.kernel_launches += 1;
-    } else if (!std::getenv("EPI_COMPACT_CUB")) {
-      const uint64_t nt = lb_tiles(n);
-      unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
-      EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
-      compact_freq_lb<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
-          d_counts, cfg.threshold, n, L, d_types, d_win, reinterpret_cast<uint32_t*>(dm + o_t),
-          reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c), lb,
-          slot_ptr(new_slot()), h_k);
-      EPI_CUDA(cudaGetLastError());
-      totals.kernel_launches += 1;
-    } else {
-      uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
-      uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
-      freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(d_counts, cfg.threshold, n, flags);
-      EPI_CUDA(cudaGetLastError());
-      dev_scan_total(flags, scan, n, new_slot(), h_k);
-      compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
-          flags, scan, n, L, d_types, d_win, d_counts, reinterpret_cast<uint32_t*>(dm + o_t),
-          reinterpret_cast<uint32_t*>(dm + o_w), reinterpret_cast<uint64_t*>(dm + o_c));
-      EPI_CUDA(cudaGetLastError());
-      totals.kernel_launches += 5;
-    }
-    g_trace.mark("compact launched");
-    prefetch_stats();
+    const bool compact_cub = std::getenv("EPI_COMPACT_CUB") != nullptr;
+    if (n > kOneBlkMax && !compact_cub) scratch_.get<unsigned long long>(kMLookback, lb_tiles(n) + 1);
+
+    // ---- device work of the level ------------------------------------------
+    auto enqueue = [&]() {
+      EPI_CUDA(cudaMemcpyAsync(d_up, h_up, up_bytes, cudaMemcpyHostToDevice, st_));
+      totals.h2d_bytes += up_bytes;
+      if (level == 2) {
+        const uint32_t* d = reinterpret_cast<const uint32_t*>(d_up);
+        gen_level2_kernel<<<blocks_for(n), 256, 0, st_>>>(d, static_cast<uint32_t>(nf), d + nf,
+                                                          d + nf + cfg.n_alpha,
+                                                          static_cast<uint32_t>(cfg.n_alpha), d_types,
+                                                          d_win, d_sigma, n);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 1;
+      } else if (level > 2) {
+        const unsigned blocks = static_cast<unsigned>((nf * 32 + 255) / 256);
+        gen_join_kernel<<<blocks, 256, 0, st_>>>(
+            L, reinterpret_cast<const uint32_t*>(d_up), reinterpret_cast<const uint32_t*>(lefts.win),
+            reinterpret_cast<const uint32_t*>(d_up + o_s), static_cast<uint32_t>(nf),
+            reinterpret_cast<const uint32_t*>(d_up + o_p), reinterpret_cast<const uint32_t*>(d_up + o_r),
+            reinterpret_cast<const uint64_t*>(d_up + o_o), d_types, d_win, d_sigma);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 1;
+      }
+      g_trace.mark("gen launched");
+      uint64_t* counts_all = d_counts;
+      if (level == 1) {
+        // single-node episodes: a popcount of each type's bitmap row
+        totals.episodes += n;
+        totals.pass2_episodes += n;
+        count_device(c, d_counts, totals, &totals.pass2_ms);
+      } else if (cnt_c > 0 && popbound) {
+        count_device_popbound(c, lefts, cfg.threshold, awin.data(), static_cast<uint32_t>(cfg.n_alpha),
+                              d_counts + lo_c, totals);
+      } else if (cnt_c > 0) {
+        count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, awin.data(),
+                              static_cast<uint32_t>(cfg.n_alpha), d_counts + lo_c, totals);
+      }
+      g_trace.mark("count launched");
+      if (sharded) {
+        // every rank's s-wide slice -> the full count vector in candidate order
+        uint64_t* d_all = scratch_.get<uint64_t>(kMGather, s * W);
+        const int rc = shard->allgather(shard->user, d_counts + static_cast<uint64_t>(R) * s, d_all,
+                                        s * sizeof(uint64_t), static_cast<void*>(st_));
+        if (rc != 0) throw Error(EPI_ENCCL, "mine: all-gather of level counts failed");
+        counts_all = d_all;
+      }
+      // threshold + compaction in candidate order, straight to host memory
+      if (n <= kOneBlkMax) {
+        compact_freq_1blk<<<1, kOneBlk, 0, st_>>>(counts_all, cfg.threshold, n, L, d_types, d_win,
+                                                  reinterpret_cast<uint32_t*>(dm + o_ft),
+                                                  reinterpret_cast<uint32_t*>(dm + o_fw),
+                                                  reinterpret_cast<uint64_t*>(dm + o_fc), slot_ptr(new_slot()),
+                                                  h_k);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 1;
+      } else if (!compact_cub) {
+        const uint64_t nt = lb_tiles(n);
+        unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
+        EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
+        compact_freq_lb<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
+            counts_all, cfg.threshold, n, L, d_types, d_win, reinterpret_cast<uint32_t*>(dm + o_ft),
+            reinterpret_cast<uint32_t*>(dm + o_fw), reinterpret_cast<uint64_t*>(dm + o_fc), lb,
+            slot_ptr(new_slot()), h_k);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 1;
+      } else {
+        uint32_t* flags = scratch_.get<uint32_t>(kMFlags, n);
+        uint32_t* scan = scratch_.get<uint32_t>(kMScan, n);
+        freq_flags_kernel<<<blocks_for(n), 256, 0, st_>>>(counts_all, cfg.threshold, n, flags);
+        EPI_CUDA(cudaGetLastError());
+        dev_scan_total(flags, scan, n, new_slot(), h_k);
+        compact_freq_kernel<<<blocks_for(n), 256, 0, st_>>>(
+            flags, scan, n, L, d_types, d_win, counts_all, reinterpret_cast<uint32_t*>(dm + o_ft),
+            reinterpret_cast<uint32_t*>(dm + o_fw), reinterpret_cast<uint64_t*>(dm + o_fc));
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 5;
+      }
+      g_trace.mark("compact launched");
+      prefetch_stats();
+    };
+
+    // key: every host-side value the enqueue depends on
+    std::string key;
+    auto put = [&](uint64_t v) { key.append(reinterpret_cast<const char*>(&v), sizeof v); };
+    put(level);
+    put(n);
+    put(nf);
+    put(lo_c);
+    put(cnt_c);
+    put(popbound);
+    put(cfg.mode);
+    put(cfg.threshold);
+    put(cfg.n_alpha);
+    for (uint32_t w : awin) put(w);
+    put(static_cast<uint64_t>(amax));
+    put(static_cast<uint64_t>(awidth));
+    put(up_bytes);
+    put(stream_.n_tiles);
+    put(stream_.blk_words);
+    put(stream_.alphabet);
+    put(stream_.gap_cap);
+    put(buffers_generation());
+    put(compact_cub);
+    put(std::getenv("EPI_WALK_SEQ") != nullptr);
+    const char* fs = std::getenv("EPI_FORCE_SEGMENTS");
+    put(fs ? std::strtoull(fs, nullptr, 10) + 1 : 0);
+    run_level(key, !sharded && !hull_pass1 && amax <= kMaxHigh, totals, enqueue);
     EPI_CUDA(cudaStreamSynchronize(st_));
     g_trace.mark("level synced");
     const uint32_t k = *reinterpret_cast<volatile uint32_t*>(h_k);
     const char* hm = static_cast<const char*>(map_out_.p);
     std::vector<uint32_t> ntypes(static_cast<size_t>(k) * L), nwin(static_cast<size_t>(k) * (L - 1));
     std::vector<uint64_t> ncnt(k);
-    std::memcpy(ntypes.data(), hm + o_t, ntypes.size() * 4);
-    std::memcpy(nwin.data(), hm + o_w, nwin.size() * 4);
-    std::memcpy(ncnt.data(), hm + o_c, ncnt.size() * 8);
+    std::memcpy(ntypes.data(), hm + o_ft, ntypes.size() * 4);
+    std::memcpy(nwin.data(), hm + o_fw, nwin.size() * 4);
+    std::memcpy(ncnt.data(), hm + o_fc, ncnt.size() * 8);
     totals.d2h_bytes += static_cast<uint64_t>(k) * (8 + 4 * (2 * L - 1)) + 4;
     record_level(n, L, ntypes.data(), nwin.data(), ncnt.data(), k,
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
