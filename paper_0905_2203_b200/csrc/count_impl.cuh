@@ -685,7 +685,12 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
     L = last;
   }
   p.counts[e] = total;
-  if (patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));
+  // statistics: one atomic per warp (per-thread atomics on one address
+  // serialise in L2)
+  const unsigned mask = __activemask();
+  const unsigned sum = __reduce_add_sync(mask, patches);
+  if (static_cast<int>(threadIdx.x & 31) == __ffs(mask) - 1 && sum)
+    atomicAdd(p.patches, static_cast<unsigned long long>(sum));
 }
 
 // Concat step, warp-parallel (few episodes, many segments): one warp per

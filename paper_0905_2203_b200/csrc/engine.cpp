@@ -394,16 +394,16 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const int64_t max_p = std::clamp<int64_t>(tiles4 / min_seg, 1, kMaxWalkSegments);
   int64_t P = 1;
   double best = 1e300;
-  // Latency regime: the launch cannot fill the SMs even at the largest P,
-  // or its live size is known only on the device (pass-2 survivors, usually
-  // few). A lone warp's concat-walk step (dependent global loads, boundary
+  // Latency regime: even at the largest P every CTA is resident at once (one
+  // wave over the resident slots), or the live size is known only on the
+  // device (pass-2 survivors, usually few). A lone warp's concat-walk step (dependent global loads, boundary
   // patches) costs about as much as kWalkLatency of its map tile steps
   // (measured on cfg2's small levels): minimise per + kWalkLatency * P.
   // Few episodes (or a device-sized set) walk warp-parallel: a segment costs
   // ~2 tile steps there instead of ~12 in the sequential walk.
   p.walk_warp = (live_slot >= 0 || n <= kWarpWalkMax) && !std::getenv("EPI_WALK_SEQ") ? 1 : 0;
   const double kWalkLatency = p.walk_warp ? 2.0 : 12.0;
-  if (live_slot >= 0 || ctas_x * max_p <= num_sms_) {
+  if (live_slot >= 0 || ctas_x * max_p <= slots) {
     for (int64_t cand = 1; cand <= max_p; ++cand) {
       const double per = static_cast<double>((tiles4 + cand - 1) / cand + (cand > 1 ? window_tiles : 0));
       const double cost = per + (cand > 1 ? kWalkLatency * static_cast<double>(cand) : 0.0);

@@ -14,6 +14,7 @@
 //      bound < threshold; singleton groups are already exact;
 //   3. pass 2: gather the survivors, count them exactly, scatter back;
 //   4. flag count >= threshold, compact in candidate order, copy back.
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 #include <cuda/atomic>
 #include <cub/device/device_radix_sort.cuh>
@@ -57,6 +58,8 @@ enum MineSlot : size_t {
   kMGather,    // all-gathered level counts (sharded mining)
   kMBound,     // pass-1 popcount bounds
   kMLookback,  // tile counter + status words of the single-pass compactions
+  kMTileCnt,   // per-tile counts of the two-launch compactions
+  kMFreqOut,   // compacted frequent set of a small level (copied back)
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -315,6 +318,140 @@ __device__ __forceinline__ void lookback_compact(uint64_t n, Pred&& pred, Emit&&
     if (bits & (1u << j)) emit(b + j, o++);
 }
 
+// ---- two-launch ordered compaction (count tiles, then emit) ------------------
+// For up to kTcMaxTiles tiles: launch 1 evaluates the predicate (with its side
+// effects) and writes one count per tile; launch 2 re-evaluates it (pure),
+// sums the counts of the preceding tiles (<= kTcMaxTiles values per CTA, no
+// inter-CTA protocol or fences) and emits in index order. Cheaper than the
+// look-back's release/acquire chain at mining-level sizes.
+constexpr uint64_t kTcMaxTiles = 2048;
+
+template <class Pred>
+__device__ __forceinline__ void tile_count(uint64_t n, Pred&& pred, uint32_t* tile_cnt) {
+  using BR = cub::BlockReduce<uint32_t, kLbThreads>;
+  __shared__ typename BR::TempStorage ts;
+  // a count needs no order: interleaved items keep loads and the
+  // predicate's side-effect stores coalesced
+  const uint64_t b = static_cast<uint64_t>(blockIdx.x) * kLbTile + threadIdx.x;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j) {
+    const uint64_t i = b + static_cast<uint64_t>(j) * kLbThreads;
+    if (i < n && pred(i)) ++cnt;
+  }
+  const uint32_t total = BR(ts).Sum(cnt);
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = total;
+}
+
+template <class Pred, class Emit>
+__device__ __forceinline__ void tile_emit(uint64_t n, Pred&& pred, Emit&& emit, const uint32_t* tile_cnt,
+                                          uint32_t* total_slot, uint32_t* host_total) {
+  using BR = cub::BlockReduce<uint32_t, kLbThreads>;
+  using BS = cub::BlockScan<uint32_t, kLbThreads>;
+  __shared__ typename BR::TempStorage tr;
+  __shared__ typename BS::TempStorage ts;
+  __shared__ uint32_t s_excl;
+  uint32_t part = 0;
+  for (uint32_t t = threadIdx.x; t < blockIdx.x; t += kLbThreads) part += tile_cnt[t];
+  const uint32_t excl = BR(tr).Sum(part);
+  if (threadIdx.x == 0) s_excl = excl;
+  // predicate with coalesced (interleaved) loads into a flag tile, then each
+  // thread takes kLbItems contiguous flags (index order for the scan)
+  __shared__ uint8_t s_flag[kLbTile];
+  const uint64_t tb = static_cast<uint64_t>(blockIdx.x) * kLbTile;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j) {
+    const uint32_t t = static_cast<uint32_t>(j) * kLbThreads + threadIdx.x;
+    s_flag[t] = (tb + t < n && pred(tb + t)) ? 1 : 0;
+  }
+  __syncthreads();
+  const uint64_t b = tb + static_cast<uint64_t>(threadIdx.x) * kLbItems;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j)
+    if (s_flag[threadIdx.x * kLbItems + j]) bits |= 1u << j;
+  uint32_t off = 0, agg = 0;
+  BS(ts).ExclusiveSum(static_cast<uint32_t>(__popc(bits)), off, agg);
+  __syncthreads();
+  const uint32_t e0 = s_excl;
+  if (threadIdx.x == 0 && blockIdx.x + 1 == gridDim.x) {
+    *total_slot = e0 + agg;
+    if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = e0 + agg;
+  }
+  uint64_t o = static_cast<uint64_t>(e0) + off;
+#pragma unroll
+  for (int j = 0; j < kLbItems; ++j)
+    if (bits & (1u << j)) emit(b + j, o++);
+}
+
+__global__ void __launch_bounds__(kLbThreads) freq_count_tc(const uint64_t* __restrict__ counts, uint64_t threshold,
+                                                            uint64_t n, uint32_t* tile_cnt) {
+  tile_count(
+      n,
+      [&](uint64_t i) {
+        const uint64_t x = counts[i];
+        return x != kPrunedDev && x >= threshold;
+      },
+      tile_cnt);
+}
+
+__global__ void __launch_bounds__(kLbThreads) freq_emit_tc(const uint64_t* __restrict__ counts, uint64_t threshold,
+                                                           uint64_t n, uint32_t L, const uint32_t* __restrict__ types,
+                                                           const uint32_t* __restrict__ win, uint32_t* otypes,
+                                                           uint32_t* owin, uint64_t* ocounts,
+                                                           const uint32_t* __restrict__ tile_cnt, uint32_t* slot,
+                                                           uint32_t* host_k) {
+  tile_emit(
+      n,
+      [&](uint64_t i) {
+        const uint64_t x = counts[i];
+        return x != kPrunedDev && x >= threshold;
+      },
+      [&](uint64_t i, uint64_t o) {
+        for (uint32_t k = 0; k < L; ++k) otypes[o * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) owin[o * (L - 1) + k] = win[i * (L - 1) + k];
+        ocounts[o] = counts[i];
+      },
+      tile_cnt, slot, host_k);
+}
+
+__global__ void __launch_bounds__(kLbThreads) prune_count_tc(const unsigned long long* __restrict__ bound,
+                                                             uint64_t threshold, uint64_t n, uint64_t* counts,
+                                                             uint32_t* tile_cnt, unsigned long long* pruned) {
+  uint32_t np = 0;
+  tile_count(
+      n,
+      [&](uint64_t i) {
+        const bool keep = bound[i] >= threshold;
+        counts[i] = keep ? 0 : kPrunedDev;
+        np += keep ? 0u : 1u;
+        return keep;
+      },
+      tile_cnt);
+  // one atomic per warp (per-thread atomics on one address serialise in L2)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+  if ((threadIdx.x & 31) == 0 && np) atomicAdd(pruned, static_cast<unsigned long long>(np));
+}
+
+__global__ void __launch_bounds__(kLbThreads) prune_emit_tc(const unsigned long long* __restrict__ bound,
+                                                            uint64_t threshold, uint64_t n, uint32_t L,
+                                                            const uint32_t* __restrict__ types,
+                                                            const uint32_t* __restrict__ win,
+                                                            const uint32_t* __restrict__ sigma, uint32_t* stypes,
+                                                            uint32_t* swin, uint32_t* ssigma, uint32_t* sidx,
+                                                            const uint32_t* __restrict__ tile_cnt, uint32_t* slot) {
+  tile_emit(
+      n, [&](uint64_t i) { return bound[i] >= threshold; },
+      [&](uint64_t i, uint64_t o) {
+        for (uint32_t k = 0; k < L; ++k) stypes[o * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) swin[o * (L - 1) + k] = win[i * (L - 1) + k];
+        ssigma[o] = sigma[i];
+        sidx[o] = static_cast<uint32_t>(i);
+      },
+      tile_cnt, slot, nullptr);
+}
+
 __global__ void __launch_bounds__(kLbThreads) compact_freq_lb(const uint64_t* __restrict__ counts,
                                                               uint64_t threshold, uint64_t n, uint32_t L,
                                                               const uint32_t* __restrict__ types,
@@ -361,7 +498,9 @@ __global__ void __launch_bounds__(kLbThreads) prune_gather_lb(const unsigned lon
         sidx[o] = static_cast<uint32_t>(i);
       },
       state, slot, nullptr);
-  if (np) atomicAdd(pruned, static_cast<unsigned long long>(np));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(0xffffffffu, np, o);
+  if ((threadIdx.x & 31) == 0 && np) atomicAdd(pruned, static_cast<unsigned long long>(np));
 }
 
 // count >= threshold (never the PRUNED sentinel) -> compacted frequent set
@@ -385,35 +524,6 @@ __global__ void __launch_bounds__(kOneBlk) compact_freq_1blk(const uint64_t* __r
       slot, host_k);
 }
 
-// pass-1 bound < threshold prunes (PRUNED sentinel); survivors gathered
-__global__ void __launch_bounds__(kOneBlk) prune_gather_1blk(const unsigned long long* __restrict__ bound,
-                                                             uint64_t threshold, uint64_t n, uint32_t L,
-                                                             const uint32_t* __restrict__ types,
-                                                             const uint32_t* __restrict__ win,
-                                                             const uint32_t* __restrict__ sigma, uint64_t* counts,
-                                                             uint32_t* stypes, uint32_t* swin, uint32_t* ssigma,
-                                                             uint32_t* sidx, uint32_t* slot,
-                                                             unsigned long long* pruned) {
-  uint32_t np = 0;
-  one_block_compact(
-      n,
-      [&](uint64_t i) { return bound[i] >= threshold; },
-      [&](uint64_t i, uint32_t o) {
-        for (uint32_t k = 0; k < L; ++k) stypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
-        for (uint32_t k = 0; k + 1 < L; ++k) swin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
-        ssigma[o] = sigma[i];
-        sidx[o] = static_cast<uint32_t>(i);
-      },
-      slot, nullptr);
-  const uint64_t chunk = (n + kOneBlk - 1) / kOneBlk;
-  const uint64_t b = min(n, threadIdx.x * chunk), e = min(n, b + chunk);
-  for (uint64_t i = b; i < e; ++i) {
-    const bool keep = bound[i] >= threshold;
-    counts[i] = keep ? 0 : kPrunedDev;
-    np += keep ? 0u : 1u;
-  }
-  if (np) atomicAdd(pruned, static_cast<unsigned long long>(np));
-}
 
 // ---- pass 1, popcount bound ------------------------------------------------
 // U(e)[t] = 1 iff some chain of e (no clears, no pe) ends at time t:
@@ -679,19 +789,6 @@ __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch 
   }
 }
 
-// bound < threshold prunes; the rest survive to pass 2.
-__global__ void prune_bound_kernel(const unsigned long long* __restrict__ bound, uint64_t threshold,
-                                   uint64_t n, uint64_t* counts, uint32_t* surv,
-                                   unsigned long long* pruned) {
-  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const bool keep = bound[i] >= threshold;
-  counts[i] = keep ? 0 : kPrunedDev;
-  surv[i] = keep ? 1u : 0u;
-  const unsigned ballot = __ballot_sync(__activemask(), !keep);
-  if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && ballot)
-    atomicAdd(pruned, static_cast<unsigned long long>(__popc(ballot)));
-}
 
 // Per sorted position: bound < threshold prunes, the rest survive to pass 2
 // (singleton groups are final when their relaxation is the episode itself).
@@ -701,20 +798,25 @@ __global__ void prune_kernel(const uint32_t* __restrict__ idx_sorted, const uint
                              bool singletons_exact, uint64_t* counts, uint32_t* surv,
                              unsigned long long* pruned) {
   const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t i = idx_sorted[j];
-  const uint32_t g = scan[j] + flags[j] - 1;
-  uint32_t s = 0;
-  if (singletons_exact && gsize[g] == 1) {
-    counts[i] = bound[g];
-  } else if (bound[g] < threshold) {
-    counts[i] = kPrunedDev;
-    atomicAdd(pruned, 1ull);
-  } else {
-    counts[i] = 0;
-    s = 1;
+  bool pr = false;
+  if (j < n) {
+    const uint32_t i = idx_sorted[j];
+    const uint32_t g = scan[j] + flags[j] - 1;
+    uint32_t s = 0;
+    if (singletons_exact && gsize[g] == 1) {
+      counts[i] = bound[g];
+    } else if (bound[g] < threshold) {
+      counts[i] = kPrunedDev;
+      pr = true;
+    } else {
+      counts[i] = 0;
+      s = 1;
+    }
+    surv[i] = s;
   }
-  surv[i] = s;
+  // one atomic per warp
+  const uint32_t bal = __ballot_sync(0xffffffffu, pr);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(pruned, static_cast<unsigned long long>(__popc(bal)));
 }
 
 __global__ void gather_kernel(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ scan,
@@ -1008,12 +1110,21 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   uint32_t* ssigma = reinterpret_cast<uint32_t*>(sbuf + s_sigma);
   uint32_t* sidx_out = reinterpret_cast<uint32_t*>(sbuf + s_idx);
   {
-    const uint64_t nt = lb_tiles(n);
-    unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
-    EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
-    prune_gather_lb<<<static_cast<unsigned>(std::max<uint64_t>(nt, 1)), kLbThreads, 0, st_>>>(
-        bound, threshold, n, L, c.types, c.win, c.sigma, d_counts, stypes, swin, ssigma, sidx_out, lb,
-        slot_ptr(mslot), d_acc_ + 2);
+    const uint64_t nt = std::max<uint64_t>(lb_tiles(n), 1);
+    if (nt <= kTcMaxTiles) {
+      uint32_t* tc = scratch_.get<uint32_t>(kMTileCnt, nt);
+      prune_count_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(bound, threshold, n, d_counts, tc,
+                                                                         d_acc_ + 2);
+      prune_emit_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(bound, threshold, n, L, c.types, c.win,
+                                                                        c.sigma, stypes, swin, ssigma, sidx_out,
+                                                                        tc, slot_ptr(mslot));
+    } else {
+      unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
+      EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
+      prune_gather_lb<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
+          bound, threshold, n, L, c.types, c.win, c.sigma, d_counts, stypes, swin, ssigma, sidx_out, lb,
+          slot_ptr(mslot), d_acc_ + 2);
+    }
     EPI_CUDA(cudaGetLastError());
     stats.kernel_launches += 3;
   }
@@ -1406,9 +1517,20 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     const size_t o_ft = 0, o_fw = align256(static_cast<size_t>(n) * L * 4),
                  o_fc = o_fw + align256(static_cast<size_t>(n) * (L - 1) * 4), o_fend = o_fc + align256(n * 8ull);
     map_out_.get(o_fend);
-    char* dm = static_cast<char*>(map_out_.d);
+    // Small levels compact into device memory and copy the (bounded) result
+    // back in one transfer; large ones write their few frequent episodes
+    // straight into mapped host memory (scattered PCIe writes are slow for
+    // thousands of entries, a full-size copy is slow for large levels).
+    constexpr size_t kCopyBack = 512u << 10;
+    const bool copy_back = o_fend <= kCopyBack;
+    char* dm = copy_back ? scratch_.get<char>(kMFreqOut, o_fend) : static_cast<char*>(map_out_.d);
     const bool compact_cub = std::getenv("EPI_COMPACT_CUB") != nullptr;
-    if (n > kOneBlkMax && !compact_cub) scratch_.get<unsigned long long>(kMLookback, lb_tiles(n) + 1);
+    if (n > kOneBlkMax && !compact_cub) {
+      if (lb_tiles(n) <= kTcMaxTiles)
+        scratch_.get<uint32_t>(kMTileCnt, lb_tiles(n));
+      else
+        scratch_.get<unsigned long long>(kMLookback, lb_tiles(n) + 1);
+    }
 
     // ---- device work of the level ------------------------------------------
     auto enqueue = [&]() {
@@ -1464,6 +1586,16 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
                                                   h_k);
         EPI_CUDA(cudaGetLastError());
         totals.kernel_launches += 1;
+      } else if (!compact_cub && lb_tiles(n) <= kTcMaxTiles) {
+        const uint64_t nt = lb_tiles(n);
+        uint32_t* tc = scratch_.get<uint32_t>(kMTileCnt, nt);
+        freq_count_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(counts_all, cfg.threshold, n, tc);
+        freq_emit_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
+            counts_all, cfg.threshold, n, L, d_types, d_win, reinterpret_cast<uint32_t*>(dm + o_ft),
+            reinterpret_cast<uint32_t*>(dm + o_fw), reinterpret_cast<uint64_t*>(dm + o_fc), tc,
+            slot_ptr(new_slot()), h_k);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 2;
       } else if (!compact_cub) {
         const uint64_t nt = lb_tiles(n);
         unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
@@ -1485,6 +1617,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
             reinterpret_cast<uint32_t*>(dm + o_fw), reinterpret_cast<uint64_t*>(dm + o_fc));
         EPI_CUDA(cudaGetLastError());
         totals.kernel_launches += 5;
+      }
+      if (copy_back) {
+        EPI_CUDA(cudaMemcpyAsync(map_out_.p, dm, o_fend, cudaMemcpyDeviceToHost, st_));
       }
       g_trace.mark("compact launched");
       prefetch_stats();
