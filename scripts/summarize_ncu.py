@@ -98,11 +98,15 @@ def launches(path):
         v = float(r[vi].replace(",", "")) / 1000.0
         tot[name] += v
         cnt[name] += 1
-    allt = sum(v for k, v in tot.items() if "probe" not in k) or 1.0
+    # the roofline probes and torch's fill kernel (the bench's L2 flush between
+    # timed steps) are not part of a step
+    def outside(k):
+        return "probe" in k or k.startswith("void at::")
+    allt = sum(v for k, v in tot.items() if not outside(k)) or 1.0
     print(f"# ncu launch list (gpu__time_duration.sum, cold, serialised): {path}")
     print(f"{'us total':>10s} {'launches':>8s} {'share':>6s}  kernel")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        share = "" if "probe" in k else f"{v / allt * 100:5.1f}%"
+        share = "" if outside(k) else f"{v / allt * 100:5.1f}%"
         print(f"{v:10.1f} {cnt[k]:8d} {share:>6s}  {k}")
 
 
