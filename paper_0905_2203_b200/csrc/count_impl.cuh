@@ -417,12 +417,19 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   const uint32_t bw = p.blk_words;
   const int stages = p.stages;
 
-  const int q = blockIdx.y;
+  // grid = (segments, episode blocks): in launches sized for an upper bound
+  // (device-side live count) the live episode blocks come first in dispatch
+  // order, so their work starts before the idle CTAs are retired
+  const int q = blockIdx.x;
   const uint32_t n_live = live_eps(p);
   // launches sized for an upper bound (device-side count): idle CTAs leave
-  if (blockIdx.x * kMachThreads >= n_live) return;
-  const uint32_t e = blockIdx.x * kMachThreads + threadIdx.x;
+  if (blockIdx.y * kMachThreads >= n_live) return;
+  const uint32_t e = blockIdx.y * kMachThreads + threadIdx.x;
   const bool active = e < n_live;
+  // warps without a live episode (a CTA's tail in small launches) keep the
+  // CTA's barrier protocol but skip the automaton: in small or device-sized
+  // launches they would otherwise multiply the SM's issue load
+  const bool warp_live = __any_sync(0xffffffffu, active);
   const int32_t gq = seg_bound(p, q);
   const int32_t gend = seg_bound(p, q + 1);
   const int32_t g0 = (gq - p.window_tiles > 0 ? gq - p.window_tiles : 0) & ~3;
@@ -522,12 +529,13 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
       dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
       // index the extern __shared__ array directly so the loads are LDS
       const uint32_t sbase = static_cast<uint32_t>(c % stages) * bw;
-      run_block(
-          gb, t0, t1,
-          [&](int k, int32_t t) { return *reinterpret_cast<const uint4*>(&stage[sbase + row_off[k] + t]); },
-          [&](int k, int32_t t) { return stage[sbase + row_off[k] + t]; });
+      if (warp_live)
+        run_block(
+            gb, t0, t1,
+            [&](int k, int32_t t) { return *reinterpret_cast<const uint4*>(&stage[sbase + row_off[k] + t]); },
+            [&](int k, int32_t t) { return stage[sbase + row_off[k] + t]; });
       __syncthreads();
-    } else {
+    } else if (warp_live) {
       const uint32_t* gbuf = p.occ + static_cast<size_t>(blk0 + c) * bw;
       run_block(
           gb, t0, t1,
@@ -802,7 +810,7 @@ void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
     *p.occ_query = blocks > 0 ? blocks : 1;
     return;
   }
-  dim3 grid((p.n_eps + kMachThreads - 1) / kMachThreads, p.P);
+  dim3 grid(p.P, (p.n_eps + kMachThreads - 1) / kMachThreads);
   machines_kernel<N, Hist><<<grid, kMachThreads, machines_smem(p), st>>>(p);
   EPI_CUDA(cudaGetLastError());
 }
