@@ -246,7 +246,7 @@ def run_ours(args, rank, world, local_rank):
 
     # Multi-GPU: each rank counts its episode shard; one all_gather of the
     # u64 counts per level over NCCL (paper_0905_2203_b200/shard.py).
-    from paper_0905_2203_b200.shard import count_sharded, make_allgather
+    from paper_0905_2203_b200.shard import make_allgather
     acc = []
 
     def count_fn(part, threshold, mode):
@@ -283,13 +283,18 @@ def run_ours(args, rank, world, local_rank):
         eps = count_candidates(args.config, args.cfg5_cands)
         csr_all = to_csr(eps)
 
+        if world > 1:
+            # epi_count_sharded: >= 4096 episodes per rank shard by episode,
+            # fewer shard the MapConcatenate segments by time
+            ag = make_allgather(memory="cuda" if coll_dev is not None else "staged", device=dev)
+
         def step():
             acc.clear()
             if world == 1:
                 count_fn(csr_all, 1, 0)
-            else:
-                count_sharded(csr_all, count_fn, device=coll_dev)
-            return merged()
+                return merged()
+            ctx.count_csr(csr_all, 1, 0, shard=(rank, world, 4096 * world, ag))
+            return len(csr_all) / world, ctx.last_stats  # job units, summed over ranks below
         workload = {"workload": f"{args.config}: exact counts of {len(eps)} "
                                 f"{len(eps[0][0])}-node candidates",
                     "events": n, "candidates": len(eps), "alphabet": alphabet}

@@ -181,6 +181,17 @@ typedef struct {
 epi_status epi_mine_sharded(epi_ctx* ctx, const epi_mine_config* cfg, const epi_shard* shard,
                             epi_mine_result* out);
 
+/* epi_count across ranks (same callback contract as epi_mine_sharded; every
+ * rank passes the same batch and receives every count). A batch of at least
+ * shard->min_shard episodes is split into `world` contiguous episode slices
+ * (counts all-gathered). A smaller batch - few episodes over a long stream -
+ * is split by TIME instead: every rank runs the MapConcatenate
+ * map step for its own contiguous block of segments, the per-segment records
+ * are all-gathered, and every rank runs the concat walk over all segments. */
+epi_status epi_count_sharded(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,
+                             uint32_t mode, const epi_shard* shard, uint64_t* counts_out,
+                             uint8_t* frequent_out, epi_stats* stats);
+
 /* Synthetic spike-train generator, a bit-exact restatement of generate()
  * (datagen.hpp:71-122): per-neuron homogeneous Poisson background plus
  * injected episodes with uniform gaps, ties ordered by neuron id. The

@@ -73,7 +73,7 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_load_stream_device", "epi_stream_size", "epi_count", "epi_mine", "epi_generate",
            "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
-           "epi_mine_sharded")
+           "epi_mine_sharded", "epi_count_sharded")
 
 
 def _load() -> C.CDLL:
@@ -95,6 +95,8 @@ def _load() -> C.CDLL:
         "epi_mine": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(MineResult)]),
         "epi_mine_sharded": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(Shard),
                                        C.POINTER(MineResult)]),
+        "epi_count_sharded": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, C.c_uint32,
+                                        C.POINTER(Shard), u64p, u8p, C.POINTER(Stats)]),
         "epi_parse_events": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), C.POINTER(i64p), u64p,
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_uint32)]),
         "epi_find_occurrences": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint32,

@@ -242,15 +242,34 @@ class Context:
                                                  C.c_void_p(d_times_ptr), n, alphabet))
 
     def count_csr(self, csr: N.CSR, threshold: int = 1, mode: int = N.MODE_EXACT,
-                  with_frequent: bool = False):
+                  with_frequent: bool = False, shard=None):
+        """epi_count; shard = (rank, world, min_shard, allgather) runs
+        epi_count_sharded (episode slices for >= min_shard episodes, time
+        segments below; see shard.make_allgather)."""
         n = len(csr)
         counts = np.zeros(n, dtype=np.uint64)
         freq = np.zeros(n, dtype=np.uint8) if with_frequent else None
         stats = N.Stats()
-        self._check(N.lib.epi_count(self._h, C.byref(csr.struct), int(threshold), int(mode),
-                                    N.ptr(counts, C.c_uint64),
-                                    N.ptr(freq, C.c_uint8) if freq is not None else None,
-                                    C.byref(stats)))
+        if shard is None:
+            self._check(N.lib.epi_count(self._h, C.byref(csr.struct), int(threshold), int(mode),
+                                        N.ptr(counts, C.c_uint64),
+                                        N.ptr(freq, C.c_uint8) if freq is not None else None,
+                                        C.byref(stats)))
+        else:
+            rank, world, min_shard, fn = shard
+
+            def _cb(user, send, recv, nbytes, stream):
+                try:
+                    return int(fn(send, recv, int(nbytes), stream) or 0)
+                except Exception as exc:  # noqa: BLE001 - reported as EPI_ENCCL
+                    self.shard_error = exc
+                    return 1
+            cb = N.ALLGATHER_FN(_cb)
+            sh = N.Shard(int(rank), int(world), int(min_shard), cb, None)
+            self._check(N.lib.epi_count_sharded(self._h, C.byref(csr.struct), int(threshold), int(mode),
+                                                C.byref(sh), N.ptr(counts, C.c_uint64),
+                                                N.ptr(freq, C.c_uint8) if freq is not None else None,
+                                                C.byref(stats)))
         self.last_stats = stats.as_dict()
         return (counts, freq) if with_frequent else counts
 

@@ -175,6 +175,16 @@ epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* o
   return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out, nullptr); });
 }
 
+epi_status epi_count_sharded(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,
+                             uint32_t mode, const epi_shard* shard, uint64_t* counts_out,
+                             uint8_t* frequent_out, epi_stats* stats) {
+  if (!ctx || !batch || !shard) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    ctx->engine.count_batch_sharded(*batch, threshold, mode, *shard, counts_out, frequent_out, stats);
+  });
+}
+
 epi_status epi_mine_sharded(epi_ctx* ctx, const epi_mine_config* cfg, const epi_shard* shard,
                             epi_mine_result* out) {
   if (!ctx || !cfg || !shard || !out) return EPI_EINVAL;

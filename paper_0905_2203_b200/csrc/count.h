@@ -37,6 +37,8 @@ struct CountLaunch {
   int* occ_query;            // host: non-null -> launch_machines* reports CTAs/SM, no launch
   uint32_t last_sh[4];       // launch_machines_last: doubling-smear shifts of the last window
   int32_t walk_warp;         // concat walk: one warp per episode (walk_warp_kernel, P <= 128)
+  int32_t q_base;            // map launch covers segments q_base .. q_base + map_segs - 1
+  int32_t map_segs;          // 0: all P segments
   const unsigned long long* hist;  // events per type (matched-pair statistics), may be null
   unsigned long long* matched;     // += sum over live episodes of sum_k hist[type_k]
 };

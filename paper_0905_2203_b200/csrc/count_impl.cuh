@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   // grid = (segments, episode blocks): in launches sized for an upper bound
   // (device-side live count) the live episode blocks come first in dispatch
   // order, so their work starts before the idle CTAs are retired
-  const int q = blockIdx.x;
+  const int q = static_cast<int>(blockIdx.x) + p.q_base;
   const uint32_t n_live = live_eps(p);
   // launches sized for an upper bound (device-side count): idle CTAs leave
   if (blockIdx.y * kMachThreads >= n_live) return;
@@ -810,7 +810,8 @@ void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
     *p.occ_query = blocks > 0 ? blocks : 1;
     return;
   }
-  dim3 grid(p.P, (p.n_eps + kMachThreads - 1) / kMachThreads);
+  // (a time shard launches only its own segments: p.map_segs of them)
+  dim3 grid(p.map_segs > 0 ? p.map_segs : p.P, (p.n_eps + kMachThreads - 1) / kMachThreads);
   machines_kernel<N, Hist><<<grid, kMachThreads, machines_smem(p), st>>>(p);
   EPI_CUDA(cudaGetLastError());
 }

@@ -28,6 +28,8 @@ enum Slot : size_t {
   kSlotMachines = 4,
   kSlotCounts = 5,
   kSlotSegments = 6,
+  kSlotShardStage = 7,
+  kSlotShardCounts = 8,
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;
@@ -432,17 +434,28 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     P = std::clamp<int64_t>(std::atoll(force), 1,
                             std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
   }
+  // Time-segment shard (epi_count_sharded with few episodes): at least one
+  // segment per rank, each rank maps its own contiguous block of segments.
+  const epi_shard* ts = (tshard_ && tshard_->world > 1 && live_slot < 0) ? tshard_ : nullptr;
+  if (ts && max_p >= static_cast<int64_t>(ts->world))
+    P = std::min<int64_t>(max_p, (std::max<int64_t>(P, ts->world) + ts->world - 1) / ts->world * ts->world);
+  else
+    ts = nullptr;  // stream too short to give every rank a segment: every rank maps all
   // Segment bounds are multiples of 4 tiles (the map kernel advances four
   // tiles per 16-byte load); the last segment runs to the 4-aligned end (the
   // bitmap is zero past the stream).
   const int64_t seg_len = ((tiles4 + P - 1) / P + 3) / 4 * 4;
   P = (tiles4 + seg_len - 1) / seg_len;
+  if (ts && P < 2) ts = nullptr;
+  const int64_t tW = ts ? ts->world : 1, tR = ts ? ts->rank : 0;
+  const int64_t s_rows = ts ? (P + tW - 1) / tW : P;  // segment rows per rank (padded)
+  const int64_t q0 = std::min<int64_t>(tR * s_rows, P), q1 = std::min<int64_t>(q0 + s_rows, P);
   // Matched-pair work of this launch (stats / roofline): sum_e sum_k n(type_k),
   // accumulated by the map kernel's first segment.
   p.hist = stream_.d_hist;
   p.matched = d_acc_ + 1;
 
-  const size_t nm = P > 1 ? static_cast<size_t>(P) * n : 1;
+  const size_t nm = P > 1 ? static_cast<size_t>(ts ? s_rows * tW : P) * n : 1;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
                m_first = align_up(m_last + nm * 8, 256), m_total = m_first + nm * 8 * kRecorded;
   char* d_mach = scratch_.get<char>(kSlotMachines, m_total);
@@ -464,9 +477,34 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   }
   Timed t{next_event(), next_event(), nullptr, ms_out, live_slot, n, tiles, true};
   rec(t.e0);
-  launch_map();
+  if (ts) {
+    p.q_base = static_cast<int32_t>(q0);
+    p.map_segs = static_cast<int32_t>(q1 - q0);
+    if (q1 > q0) launch_map();
+    p.q_base = 0;
+    p.map_segs = 0;
+  } else {
+    launch_map();
+  }
   rec(t.e_map);
   t.e1 = t.e_map;
+  if (ts) {
+    // all-gather the segment records (q-major rows): every rank then walks
+    // all P segments and gets every count
+    struct Field {
+      void* base;
+      size_t elem;
+    } fields[4] = {{p.f_count, 4}, {p.f_ncomp, 4}, {p.f_last, 8}, {p.f_first, 8ull * kRecorded}};
+    const size_t row_bytes_max = static_cast<size_t>(s_rows) * n * 8 * kRecorded;
+    char* stage = scratch_.get<char>(kSlotShardStage, row_bytes_max);
+    for (const Field& f : fields) {
+      const size_t bytes = static_cast<size_t>(s_rows) * n * f.elem;
+      EPI_CUDA(cudaMemcpyAsync(stage, static_cast<char*>(f.base) + static_cast<size_t>(tR * s_rows) * n * f.elem,
+                               bytes, cudaMemcpyDeviceToDevice, st_));
+      if (ts->allgather(ts->user, stage, f.base, bytes, static_cast<void*>(st_)) != 0)
+        throw Error(EPI_ENCCL, "count: all-gather of segment records failed");
+    }
+  }
   if (P > 1) {
     if (wide)
       launch_walk_wide(static_cast<int>(N), p, st_);
@@ -619,6 +657,60 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
       frequent_out[e] = counts_out[e] != kPruned && counts_out[e] >= threshold;
   flush_stats(stats);
   if (stats_out) *stats_out = stats;
+}
+
+void Engine::count_batch_sharded(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
+                                 const epi_shard& shard, uint64_t* counts_out, uint8_t* frequent_out,
+                                 epi_stats* stats_out) {
+  const uint64_t n = b.n_episodes;
+  const uint64_t W = shard.world, R = shard.rank;
+  if (W == 0 || R >= W || (W > 1 && !shard.allgather))
+    throw Error(EPI_EINVAL, "count: invalid shard (rank, world, allgather)");
+  if (W == 1) {
+    count_batch(b, threshold, mode, counts_out, frequent_out, stats_out);
+    return;
+  }
+  if (n && (!b.offsets || !counts_out)) throw Error(EPI_EINVAL, "epi_count: null batch arrays");
+  if (n >= std::max<uint64_t>(shard.min_shard, W * W)) {
+    // episode shards: count slice [R*s, R*s + s) locally, all-gather the counts
+    const uint64_t s = (n + W - 1) / W;
+    const uint64_t lo = std::min(R * s, n), hi = std::min(lo + s, n);
+    std::vector<uint32_t> off(hi - lo + 1, 0), ty;
+    std::vector<int64_t> low, high;
+    for (uint64_t e = lo; e < hi; ++e) {
+      if (b.offsets[e + 1] < b.offsets[e]) throw Error(EPI_EINVAL, "epi_count: offsets not monotone");
+      const uint32_t b0 = b.offsets[e], N = b.offsets[e + 1] - b0;
+      ty.insert(ty.end(), b.types + b0, b.types + b0 + N);
+      if (N > 1) {
+        low.insert(low.end(), b.low + (b0 - e), b.low + (b0 - e) + N - 1);
+        high.insert(high.end(), b.high + (b0 - e), b.high + (b0 - e) + N - 1);
+      }
+      off[e - lo + 1] = static_cast<uint32_t>(ty.size());
+    }
+    const epi_episode_batch sub{hi - lo, off.data(), ty.data(), low.data(), high.data()};
+    std::vector<uint64_t> local(hi - lo);
+    count_batch(sub, threshold, mode, local.data(), nullptr, stats_out);
+    uint64_t* d = scratch_.get<uint64_t>(kSlotShardCounts, s * (W + 1));
+    uint64_t* d_send = d + s * W;
+    EPI_CUDA(cudaMemsetAsync(d_send, 0, s * sizeof(uint64_t), st_));
+    if (hi > lo)
+      EPI_CUDA(cudaMemcpyAsync(d_send, local.data(), (hi - lo) * sizeof(uint64_t), cudaMemcpyHostToDevice, st_));
+    if (shard.allgather(shard.user, d_send, d, s * sizeof(uint64_t), static_cast<void*>(st_)) != 0)
+      throw Error(EPI_ENCCL, "count: all-gather of counts failed");
+    EPI_CUDA(cudaMemcpyAsync(counts_out, d, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st_));
+    EPI_CUDA(cudaStreamSynchronize(st_));
+  } else {
+    // time shards: every rank counts every episode over its own segments
+    struct Guard {
+      const epi_shard*& slot;
+      ~Guard() { slot = nullptr; }
+    } guard{tshard_};
+    tshard_ = &shard;
+    count_batch(b, threshold, mode, counts_out, nullptr, stats_out);
+  }
+  if (frequent_out)
+    for (uint64_t e = 0; e < n; ++e)
+      frequent_out[e] = counts_out[e] != kPruned && counts_out[e] >= threshold;
 }
 
 // generate_candidates (E/miner.hpp:76-109). `frequent` holds the level-1

@@ -105,6 +105,12 @@ class Engine {
                    uint64_t* counts_out, uint8_t* frequent_out, epi_stats* stats);
   // shard == nullptr: single device (epi_mine); else epi_mine_sharded.
   void mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_shard* shard);
+  // epi_count_sharded: many episodes -> episode slices + all-gather of the
+  // counts; few episodes -> MapConcatenate segments sharded by time range,
+  // the segment records all-gathered and walked on every rank.
+  void count_batch_sharded(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
+                           const epi_shard& shard, uint64_t* counts_out, uint8_t* frequent_out,
+                           epi_stats* stats);
   // Parallel local tracking (tracking.cu): counts (greedy) and/or intervals.
   void track_batch(const epi_episode_batch& b, uint32_t direction, uint64_t* counts_out,
                    std::vector<uint64_t>* off_out, std::vector<int64_t>* starts,
@@ -156,6 +162,7 @@ class Engine {
   // nothing was launched in between.
   void prefetch_stats();
   uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
+  const epi_shard* tshard_ = nullptr;  // active time-segment shard (count_device)
 
   cudaEvent_t next_event();
   int new_slot();  // a device u32 log slot, unique within the call

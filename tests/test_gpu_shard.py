@@ -138,3 +138,79 @@ def test_allgather_callback_nccl_plumbing():
         assert torch.equal(send, recv)
     finally:
         dist.destroy_process_group()
+
+
+def _threaded(world, fn_per_rank):
+    """Run fn_per_rank(rank, allgather_fn) in `world` threads with a barrier
+    all-gather over device pointers; returns the per-rank results."""
+    import torch
+    barrier = threading.Barrier(world)
+    slices, out, errs = {}, [None] * world, []
+
+    def make_fn(r):
+        def fn(send, recv, nbytes, stream):
+            torch.cuda.ExternalStream(int(stream)).synchronize()
+            slices[r] = torch.as_tensor(_RawDevice(send, nbytes), device="cuda").clone()
+            barrier.wait()
+            dst = torch.as_tensor(_RawDevice(recv, nbytes * world), device="cuda")
+            dst.copy_(torch.cat([slices[q] for q in range(world)]))
+            torch.cuda.synchronize()
+            barrier.wait()
+            return 0
+        return fn
+
+    def run(r):
+        try:
+            out[r] = fn_per_rank(r, make_fn(r))
+        except Exception as exc:
+            errs.append(exc)
+            barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", ["time", "time_mine", "time_forced", "episode"])
+def test_sharded_count_equals_unsharded(ctx, world, case, monkeypatch):
+    """epi_count_sharded: few episodes over a long stream shard the
+    MapConcatenate segments by time (records all-gathered, walked on every
+    rank); many episodes shard by episode. Every rank's counts == the
+    unsharded device counts (and the oracle port on a subset)."""
+    import oracle
+    from helpers import csr_of
+    from paper_0905_2203_b200 import GenConfig, generate_arrays
+    types, times = generate_arrays(GenConfig(64, 1_000_000 / (64 * 20), 20, [], 51))
+    rng = np.random.default_rng(world)
+    nep = 2000 if case == "episode" else 40
+    eps = [([int(x) for x in rng.integers(0, 64, 3)], [BINS[int(b)] for b in rng.integers(0, 3, 2)])
+           for _ in range(nep)]
+    csr = csr_of(eps)
+    mode = MODE_MINE if case == "time_mine" else MODE_EXACT
+    thr = 40 if case == "time_mine" else 1
+    if case == "time_forced":
+        monkeypatch.setenv("EPI_FORCE_SEGMENTS", "7")
+    ctx.load_arrays(types, times, 64)
+    want = ctx.count_csr(csr, thr, mode)
+
+    def per_rank(r, fn):
+        c = Context(0)
+        c.load_arrays(types, times, 64)
+        got = c.count_csr(csr, thr, mode, shard=(r, world, 1000, fn))
+        st = c.last_stats
+        c.close()
+        return got, st
+    res = _threaded(world, per_rank)
+    for r, (got, st) in enumerate(res):
+        np.testing.assert_array_equal(got, want, err_msg=f"rank {r}")
+        if case.startswith("time"):
+            assert st["segments"] >= world
+    sub = csr_of(eps[:8])
+    exact = oracle.count_batch(types, times, sub.offsets, sub.types, sub.low, sub.high, threads=8)
+    if mode == MODE_EXACT:
+        np.testing.assert_array_equal(res[0][0][:8], exact)
