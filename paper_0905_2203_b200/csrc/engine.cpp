@@ -79,8 +79,10 @@ Engine::Engine(int device) : device_(device) {
   EPI_CUDA(cudaEventCreate(&ev0_));
   EPI_CUDA(cudaEventCreate(&ev1_));
   EPI_CUDA(cudaEventCreate(&ev2_));
-  EPI_CUDA(cudaMalloc(&d_log_, kLogSlots * sizeof(uint32_t)));
-  EPI_CUDA(cudaMalloc(&d_acc_, 4 * sizeof(unsigned long long)));
+  // one allocation: 64 bytes of accumulators, then the log slots, so the
+  // statistics come back in one copy (same layout as the pinned mirror)
+  EPI_CUDA(cudaMalloc(&d_acc_, 64 + kLogSlots * sizeof(uint32_t)));
+  d_log_ = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(d_acc_) + 64);
   EPI_CUDA(cudaMemset(d_acc_, 0, 4 * sizeof(unsigned long long)));
 }
 
@@ -93,8 +95,7 @@ Engine::~Engine() {
   if (ev1_) cudaEventDestroy(ev1_);
   if (ev2_) cudaEventDestroy(ev2_);
   for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
-  if (d_log_) cudaFree(d_log_);
-  if (d_acc_) cudaFree(d_acc_);
+  if (d_acc_) cudaFree(d_acc_);  // (d_log_ lives in the same allocation)
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -137,8 +138,7 @@ int Engine::new_slot() {
 void Engine::prefetch_stats() {
   const size_t nlog = static_cast<size_t>(log_used_);
   char* h = static_cast<char*>(pin_small_.get(64 + kLogSlots * sizeof(uint32_t)));
-  EPI_CUDA(cudaMemcpyAsync(h, d_acc_, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st_));
-  if (nlog) EPI_CUDA(cudaMemcpyAsync(h + 64, d_log_, nlog * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaMemcpyAsync(h, d_acc_, 64 + nlog * sizeof(uint32_t), cudaMemcpyDeviceToHost, st_));
   prefetched_epoch_ = stat_epoch_;
 }
 

@@ -163,6 +163,7 @@ class Engine {
   void prefetch_stats();
   uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
   const epi_shard* tshard_ = nullptr;  // active time-segment shard (count_device)
+  uint64_t iota_n_ = 0;                 // size of the level-1 type-id buffer
 
   cudaEvent_t next_event();
   int new_slot();  // a device u32 log slot, unique within the call

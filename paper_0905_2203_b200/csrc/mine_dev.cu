@@ -60,6 +60,7 @@ enum MineSlot : size_t {
   kMLookback,  // tile counter + status words of the single-pass compactions
   kMTileCnt,   // per-tile counts of the two-launch compactions
   kMFreqOut,   // compacted frequent set of a small level (copied back)
+  kMIota,      // level-1 candidates: type ids 0..A-1
 };
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
@@ -1455,10 +1456,17 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     char* d_up = nullptr;
     size_t o_s = 0, o_p = 0, o_r = 0, o_o = 0;  // join upload layout (level >= 3)
     if (level == 1) {
-      up_bytes = n * 4;
-      h_up = static_cast<char*>(pin_up_.get(up_bytes));
-      std::iota(reinterpret_cast<uint32_t*>(h_up), reinterpret_cast<uint32_t*>(h_up) + n, 0u);
-      d_up = reinterpret_cast<char*>(d_types);
+      // the level-1 candidates are the type ids 0..A-1: a persistent device
+      // copy (filled when the alphabet size changes), no per-call upload
+      if (iota_n_ != n) {
+        uint32_t* d = scratch_.get<uint32_t>(kMIota, n);
+        std::vector<uint32_t> h(n);
+        std::iota(h.begin(), h.end(), 0u);
+        EPI_CUDA(cudaMemcpyAsync(d, h.data(), n * 4, cudaMemcpyHostToDevice, st_));
+        EPI_CUDA(cudaStreamSynchronize(st_));
+        iota_n_ = n;
+      }
+      d_types = scratch_.get<uint32_t>(kMIota, n);
     } else if (level == 2) {
       const size_t up = nf + 2 * cfg.n_alpha;
       up_bytes = up * 4;
@@ -1534,8 +1542,10 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
 
     // ---- device work of the level ------------------------------------------
     auto enqueue = [&]() {
-      EPI_CUDA(cudaMemcpyAsync(d_up, h_up, up_bytes, cudaMemcpyHostToDevice, st_));
-      totals.h2d_bytes += up_bytes;
+      if (up_bytes) {
+        EPI_CUDA(cudaMemcpyAsync(d_up, h_up, up_bytes, cudaMemcpyHostToDevice, st_));
+        totals.h2d_bytes += up_bytes;
+      }
       if (level == 2) {
         const uint32_t* d = reinterpret_cast<const uint32_t*>(d_up);
         gen_level2_kernel<<<blocks_for(n), 256, 0, st_>>>(d, static_cast<uint32_t>(nf), d + nf,
