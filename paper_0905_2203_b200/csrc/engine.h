@@ -144,9 +144,20 @@ class Engine {
     uint64_t stride = 0;
     uint64_t slice_lo = 0;
   };
+  // Survivors of pass 1 and their exact counts (device; live count in log
+  // slot `slot`): what the frequent-set compaction needs when the level's
+  // full count vector is not (unsharded mining).
+  struct Survivors {
+    const uint32_t* types = nullptr;
+    const uint32_t* win = nullptr;
+    const uint64_t* counts = nullptr;
+    int slot = -1;
+  };
+  // surv != nullptr: skip scattering the survivors' counts back into
+  // d_counts and report the survivors instead.
   void count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t threshold,
                              const uint32_t* alpha, uint32_t n_alpha, uint64_t* d_counts,
-                             epi_stats& stats);
+                             epi_stats& stats, Survivors* surv = nullptr);
   // Exclusive scan of n u32 flags; the total goes to device log slot `slot`
   // (and to *host_total, zero-copy, when given). No host synchronisation.
   void dev_scan_total(const uint32_t* flags, uint32_t* scan, uint64_t n, int slot,

@@ -329,6 +329,7 @@ constexpr uint64_t kTcMaxTiles = 2048;
 
 template <class Pred>
 __device__ __forceinline__ void tile_count(uint64_t n, Pred&& pred, uint32_t* tile_cnt) {
+  // (callers with a device-side item count pass it as n; tiles past it count 0)
   using BR = cub::BlockReduce<uint32_t, kLbThreads>;
   __shared__ typename BR::TempStorage ts;
   // a count needs no order: interleaved items keep loads and the
@@ -375,7 +376,9 @@ __device__ __forceinline__ void tile_emit(uint64_t n, Pred&& pred, Emit&& emit, 
   BS(ts).ExclusiveSum(static_cast<uint32_t>(__popc(bits)), off, agg);
   __syncthreads();
   const uint32_t e0 = s_excl;
-  if (threadIdx.x == 0 && blockIdx.x + 1 == gridDim.x) {
+  // the tile holding item n-1 (tile 0 when n == 0) knows the total
+  const uint64_t last_tile = n ? (n - 1) / kLbTile : 0;
+  if (threadIdx.x == 0 && blockIdx.x == last_tile) {
     *total_slot = e0 + agg;
     if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = e0 + agg;
   }
@@ -408,6 +411,32 @@ __global__ void __launch_bounds__(kLbThreads) freq_emit_tc(const uint64_t* __res
         const uint64_t x = counts[i];
         return x != kPrunedDev && x >= threshold;
       },
+      [&](uint64_t i, uint64_t o) {
+        for (uint32_t k = 0; k < L; ++k) otypes[o * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) owin[o * (L - 1) + k] = win[i * (L - 1) + k];
+        ocounts[o] = counts[i];
+      },
+      tile_cnt, slot, host_k);
+}
+
+// Frequent episodes among pass-1 survivors (device-side survivor count
+// *m_dev; the grid covers an upper bound): survivors are in candidate order,
+// and pruned candidates are never frequent, so this is the level's frequent
+// set in candidate order.
+__global__ void __launch_bounds__(kLbThreads) surv_count_tc(const uint64_t* __restrict__ counts, uint64_t threshold,
+                                                            const uint32_t* __restrict__ m_dev, uint32_t* tile_cnt) {
+  tile_count(*m_dev, [&](uint64_t i) { return counts[i] >= threshold; }, tile_cnt);
+}
+
+__global__ void __launch_bounds__(kLbThreads) surv_emit_tc(const uint64_t* __restrict__ counts, uint64_t threshold,
+                                                           const uint32_t* __restrict__ m_dev, uint32_t L,
+                                                           const uint32_t* __restrict__ types,
+                                                           const uint32_t* __restrict__ win, uint32_t* otypes,
+                                                           uint32_t* owin, uint64_t* ocounts,
+                                                           const uint32_t* __restrict__ tile_cnt, uint32_t* slot,
+                                                           uint32_t* host_k) {
+  tile_emit(
+      *m_dev, [&](uint64_t i) { return counts[i] >= threshold; },
       [&](uint64_t i, uint64_t o) {
         for (uint32_t k = 0; k < L; ++k) otypes[o * L + k] = types[i * L + k];
         for (uint32_t k = 0; k + 1 < L; ++k) owin[o * (L - 1) + k] = win[i * (L - 1) + k];
@@ -1035,7 +1064,7 @@ void Engine::count_device_two_pass(const DevSet& c, uint64_t threshold, uint32_t
 // not wait: survivors are sized on the device.
 void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t threshold,
                                    const uint32_t* alpha, uint32_t n_alpha, uint64_t* d_counts,
-                                   epi_stats& stats) {
+                                   epi_stats& stats, Survivors* surv) {
   const uint64_t n = c.n;
   const uint32_t L = c.N, M = L - 1;
   stats.episodes += n;
@@ -1135,6 +1164,13 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   sv.sigma = ssigma;
   uint64_t* sc = scratch_.get<uint64_t>(kMSurvCnt, n);
   count_device(sv, sc, stats, &stats.pass2_ms, mslot);
+  if (surv) {
+    surv->types = stypes;
+    surv->win = swin;
+    surv->counts = sc;
+    surv->slot = mslot;
+    return;
+  }
   scatter_counts_kernel<<<blocks_for(n), 256, 0, st_>>>(sidx_out, sc, slot_ptr(mslot), d_counts);
   EPI_CUDA(cudaGetLastError());
   stats.kernel_launches += 2;
@@ -1540,8 +1576,11 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         scratch_.get<unsigned long long>(kMLookback, lb_tiles(n) + 1);
     }
 
+    if (popbound) scratch_.get<uint32_t>(kMTileCnt, std::max<uint64_t>(lb_tiles(n), 1));
+    Survivors surv;  // set by the popbound pass on unsharded levels
     // ---- device work of the level ------------------------------------------
     auto enqueue = [&]() {
+      surv = Survivors{};
       if (up_bytes) {
         EPI_CUDA(cudaMemcpyAsync(d_up, h_up, up_bytes, cudaMemcpyHostToDevice, st_));
         totals.h2d_bytes += up_bytes;
@@ -1573,7 +1612,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         count_device(c, d_counts, totals, &totals.pass2_ms);
       } else if (cnt_c > 0 && popbound) {
         count_device_popbound(c, lefts, cfg.threshold, awin.data(), static_cast<uint32_t>(cfg.n_alpha),
-                              d_counts + lo_c, totals);
+                              d_counts + lo_c, totals, sharded ? nullptr : &surv);
       } else if (cnt_c > 0) {
         count_device_two_pass(c, cfg.threshold, cfg.mode, alpha_hull, awin.data(),
                               static_cast<uint32_t>(cfg.n_alpha), d_counts + lo_c, totals);
@@ -1588,7 +1627,19 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         counts_all = d_all;
       }
       // threshold + compaction in candidate order, straight to host memory
-      if (n <= kOneBlkMax) {
+      if (surv.slot >= 0) {
+        // only pass-1 survivors can be frequent: compact those (in order)
+        const uint64_t nt = std::max<uint64_t>(lb_tiles(n), 1);
+        uint32_t* tc = scratch_.get<uint32_t>(kMTileCnt, nt);
+        surv_count_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(surv.counts, cfg.threshold,
+                                                                         slot_ptr(surv.slot), tc);
+        surv_emit_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(
+            surv.counts, cfg.threshold, slot_ptr(surv.slot), L, surv.types, surv.win,
+            reinterpret_cast<uint32_t*>(dm + o_ft), reinterpret_cast<uint32_t*>(dm + o_fw),
+            reinterpret_cast<uint64_t*>(dm + o_fc), tc, slot_ptr(new_slot()), h_k);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 2;
+      } else if (n <= kOneBlkMax) {
         compact_freq_1blk<<<1, kOneBlk, 0, st_>>>(counts_all, cfg.threshold, n, L, d_types, d_win,
                                                   reinterpret_cast<uint32_t*>(dm + o_ft),
                                                   reinterpret_cast<uint32_t*>(dm + o_fw),
