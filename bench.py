@@ -387,6 +387,10 @@ def run_ours(args, rank, world, local_rank):
                                                             if kernel == "machines_kernel" else None)
         return (tj["dram_bytes_per_launch"], tj["source"]) if tj else (None, None)
 
+    def pipes_for(kernel):
+        tj = traffic_all.get(f"{args.config}:{kernel}")
+        return tj.get("pipe_util") if tj else None
+
     kernels = []
     if map_ms > 0:
         ach = matched / (map_ms * 1e-3) / 1e12
@@ -397,6 +401,7 @@ def run_ours(args, rank, world, local_rank):
                         "frac": round(ach / peak_int, 5) if peak_int else None,
                         "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": src,
                         "peak_source": "epi_probe_int32 mode 1 (LOP3+IMAD, measured in this run)",
+                        "pipe_util_ncu": pipes_for("machines_kernel"),
                         "launches": map_launches, "avg_launch_ms": round(map_ms / max(map_launches, 1), 5),
                         "device_ms": round(map_ms, 4),
                         "share_of_device_time": round(map_ms / total_dev_ms, 4) if total_dev_ms else None,
@@ -411,6 +416,7 @@ def run_ours(args, rank, world, local_rank):
                         "frac": round(ach / peak_popc, 5) if peak_popc else None,
                         "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": src,
                         "peak_source": "epi_probe_int32 mode 2 (POPC, XU pipe, measured in this run)",
+                        "pipe_util_ncu": pipes_for("bound_kernel"),
                         "device_ms": round(bound_ms, 4),
                         "share_of_device_time": round(bound_ms / total_dev_ms, 4) if total_dev_ms else None})
     kernels.sort(key=lambda k: -k["device_ms"])

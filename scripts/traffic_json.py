@@ -24,8 +24,16 @@ for cfg, rep, summary in CAPTURES:
         def nbytes(name):
             u, v = col[name]
             return float(v.replace(",", "")) * SCALE[u]
+        def pct(name):
+            try:
+                return round(float(col[name][1].replace(",", "")) / 100.0, 4)
+            except (KeyError, ValueError):
+                return None
         out[cfg] = {"kernel": col.get("Kernel Name", ("", ""))[1],
                     "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
+                    # issue utilisation of the integer pipes (fraction of peak, ncu)
+                    "pipe_util": {k: pct(f"sm__inst_executed_pipe_{k}.avg.pct_of_peak_sustained_active")
+                                  for k in ("alu", "fma", "xu", "lsu")},
                     "source": summary}
     except Exception as e:  # capture missing
         print(cfg, "skipped:", e, file=sys.stderr)
