@@ -417,14 +417,17 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   const uint32_t bw = p.blk_words;
   const int stages = p.stages;
 
-  // grid = (segments, episode blocks): in launches sized for an upper bound
-  // (device-side live count) the live episode blocks come first in dispatch
-  // order, so their work starts before the idle CTAs are retired
-  const int q = static_cast<int>(blockIdx.x) + p.q_base;
+  // Grid: (episode blocks, segments) - CTAs resident together walk the same
+  // segments, so each staged bitmap block is reused from L2 across episode
+  // blocks. Launches sized for an upper bound (device-side live count) use
+  // (segments, episode blocks) instead: the live episode blocks come first in
+  // dispatch order and start before the idle CTAs are retired.
+  const int q = static_cast<int>(p.n_dev ? blockIdx.x : blockIdx.y) + p.q_base;
+  const uint32_t eblk = p.n_dev ? blockIdx.y : blockIdx.x;
   const uint32_t n_live = live_eps(p);
   // launches sized for an upper bound (device-side count): idle CTAs leave
-  if (blockIdx.y * kMachThreads >= n_live) return;
-  const uint32_t e = blockIdx.y * kMachThreads + threadIdx.x;
+  if (eblk * kMachThreads >= n_live) return;
+  const uint32_t e = eblk * kMachThreads + threadIdx.x;
   const bool active = e < n_live;
   // warps without a live episode (a CTA's tail in small launches) keep the
   // CTA's barrier protocol but skip the automaton: in small or device-sized
@@ -811,7 +814,9 @@ void launch_machines_n(const CountLaunch& p, cudaStream_t st) {
     return;
   }
   // (a time shard launches only its own segments: p.map_segs of them)
-  dim3 grid(p.map_segs > 0 ? p.map_segs : p.P, (p.n_eps + kMachThreads - 1) / kMachThreads);
+  const unsigned segs = static_cast<unsigned>(p.map_segs > 0 ? p.map_segs : p.P);
+  const unsigned eblks = (p.n_eps + kMachThreads - 1) / kMachThreads;
+  const dim3 grid = p.n_dev ? dim3(segs, eblks) : dim3(eblks, segs);
   machines_kernel<N, Hist><<<grid, kMachThreads, machines_smem(p), st>>>(p);
   EPI_CUDA(cudaGetLastError());
 }
