@@ -54,6 +54,27 @@ class MineConfig(C.Structure):
                 ("alpha_high", i64p), ("n_alpha", C.c_uint64), ("mode", C.c_uint32)]
 
 
+class EpisodeBatchOut(C.Structure):
+    """EpisodeBatch as written by the library (raw addresses: cheap to copy out)."""
+    _fields_ = [("n_episodes", C.c_uint64), ("offsets", C.c_void_p), ("types", C.c_void_p),
+                ("low", C.c_void_p), ("high", C.c_void_p)]
+
+
+class MineResultOut(C.Structure):
+    """epi_mine_result with raw-address fields (same layout as MineResult)."""
+    _fields_ = [("n_levels", C.c_uint64), ("level_candidates", C.c_void_p), ("level_offsets", C.c_void_p),
+                ("level_ms", C.c_void_p), ("frequent", EpisodeBatchOut), ("counts", C.c_void_p),
+                ("totals", Stats)]
+
+
+def copy_addr(addr, count: int, dtype) -> np.ndarray:
+    """Copy `count` elements at a library-owned address into a new array."""
+    if not count:
+        return np.zeros(0, dtype=dtype)
+    dt = np.dtype(dtype)
+    return np.frombuffer(C.string_at(addr, count * dt.itemsize), dtype=dt).copy()
+
+
 class MineResult(C.Structure):
     _fields_ = [("n_levels", C.c_uint64), ("level_candidates", u64p), ("level_offsets", u64p),
                 ("level_ms", f64p), ("frequent", EpisodeBatch), ("counts", u64p),
@@ -92,9 +113,9 @@ def _load() -> C.CDLL:
         "epi_stream_size": (C.c_uint64, [C.c_void_p]),
         "epi_count": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, C.c_uint32, u64p, u8p,
                                 C.POINTER(Stats)]),
-        "epi_mine": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(MineResult)]),
+        "epi_mine": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(MineResultOut)]),
         "epi_mine_sharded": (C.c_int, [C.c_void_p, C.POINTER(MineConfig), C.POINTER(Shard),
-                                       C.POINTER(MineResult)]),
+                                       C.POINTER(MineResultOut)]),
         "epi_count_sharded": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, C.c_uint32,
                                         C.POINTER(Shard), u64p, u8p, C.POINTER(Stats)]),
         "epi_parse_events": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), C.POINTER(i64p), u64p,

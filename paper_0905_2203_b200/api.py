@@ -317,7 +317,7 @@ class Context:
             cfg_ = N.MineConfig(key[1], key[2], N.ptr(lo, C.c_int64), N.ptr(hi, C.c_int64), len(bins), key[3])
             self._mine_cfg = cached = (key, cfg_, lo, hi)  # arrays kept alive with the struct
         cfg = cached[1]
-        res = N.MineResult()
+        res = N.MineResultOut()
         if shard is None:
             self._check(N.lib.epi_mine(self._h, C.byref(cfg), C.byref(res)))
         else:
@@ -333,11 +333,20 @@ class Context:
             sh = N.Shard(int(rank), int(world), int(min_shard), cb, None)
             self._check(N.lib.epi_mine_sharded(self._h, C.byref(cfg), C.byref(sh), C.byref(res)))
         nl = int(res.n_levels)
-        cands = N.copy_out(res.level_candidates, nl, np.uint64).tolist()
-        offs = N.copy_out(res.level_offsets, nl + 1, np.uint64).tolist()
-        ms = N.copy_out(res.level_ms, nl, np.float64).tolist()
-        csr = N.CSR.from_struct(res.frequent)
-        counts = N.copy_out(res.counts, len(csr), np.uint64)
+        cands = N.copy_addr(res.level_candidates, nl, np.uint64).tolist()
+        offs = N.copy_addr(res.level_offsets, nl + 1, np.uint64).tolist()
+        ms = N.copy_addr(res.level_ms, nl, np.float64).tolist()
+        fr = res.frequent
+        nf = int(fr.n_episodes)
+        if nf:
+            off = N.copy_addr(fr.offsets, nf + 1, np.uint32)
+            nt = int(off[-1])
+            csr = N.CSR(off, N.copy_addr(fr.types, nt, np.uint32), N.copy_addr(fr.low, nt - nf, np.int64),
+                        N.copy_addr(fr.high, nt - nf, np.int64))
+        else:
+            csr = N.CSR(np.zeros(1, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.int64),
+                        np.zeros(0, np.int64))
+        counts = N.copy_addr(res.counts, nf, np.uint64)
         return cands, offs, ms, csr, counts, res.totals.as_dict()
 
 
