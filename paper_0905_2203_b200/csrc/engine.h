@@ -143,6 +143,12 @@ class Engine {
     const uint64_t* off = nullptr;
     uint64_t stride = 0;
     uint64_t slice_lo = 0;
+    // join mode: the level's candidates were not materialised (no
+    // gen_join_kernel); the passes read them off the join index
+    bool join_mode = false;
+    const uint32_t* pre = nullptr;     // bucket order of the rights
+    const uint32_t* lrange = nullptr;  // [2 nf] bucket range per left
+    const uint32_t* sigma = nullptr;   // [nf] lefts' sums of highs
   };
   // Survivors of pass 1 and their exact counts (device; live count in log
   // slot `slot`): what the frequent-set compaction needs when the level's

@@ -319,6 +319,20 @@ __device__ __forceinline__ void lookback_compact(uint64_t n, Pred&& pred, Emit&&
     if (bits & (1u << j)) emit(b + j, o++);
 }
 
+// Join-mode candidate (global index i): its left (binary search over loff)
+// and right.
+__device__ __forceinline__ void join_pair(const uint64_t* __restrict__ loff, uint32_t nf,
+                                          const uint32_t* __restrict__ pre, const uint32_t* __restrict__ lrange,
+                                          uint64_t i, uint32_t& l, uint32_t& r) {
+  uint32_t lo = 0, hi = nf;  // largest l with loff[l] <= i
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (loff[mid] <= i) lo = mid; else hi = mid;
+  }
+  l = lo;
+  r = pre[lrange[2 * l] + static_cast<uint32_t>(i - loff[l])];
+}
+
 // ---- two-launch ordered compaction (count tiles, then emit) ------------------
 // For up to kTcMaxTiles tiles: launch 1 evaluates the predicate (with its side
 // effects) and writes one count per tile; launch 2 re-evaluates it (pure),
@@ -464,19 +478,45 @@ __global__ void __launch_bounds__(kLbThreads) prune_count_tc(const unsigned long
   if ((threadIdx.x & 31) == 0 && np) atomicAdd(pruned, static_cast<unsigned long long>(np));
 }
 
+// Join index of a level (join mode of the popcount pass): lefts' types and
+// windows, their sums of highs, and the bucket order / ranges / offsets.
+struct JoinIdx {
+  const uint32_t* ftypes;  // [nf * F]
+  const uint32_t* fwin;    // [nf * (F-1)]
+  const uint32_t* fsigma;  // [nf]
+  const uint32_t* pre;
+  const uint32_t* lrange;
+  const uint64_t* loff;
+  uint32_t nf, F;
+};
+
 __global__ void __launch_bounds__(kLbThreads) prune_emit_tc(const unsigned long long* __restrict__ bound,
                                                             uint64_t threshold, uint64_t n, uint32_t L,
                                                             const uint32_t* __restrict__ types,
                                                             const uint32_t* __restrict__ win,
                                                             const uint32_t* __restrict__ sigma, uint32_t* stypes,
                                                             uint32_t* swin, uint32_t* ssigma, uint32_t* sidx,
-                                                            const uint32_t* __restrict__ tile_cnt, uint32_t* slot) {
+                                                            const uint32_t* __restrict__ tile_cnt, uint32_t* slot,
+                                                            const JoinIdx jx) {
   tile_emit(
       n, [&](uint64_t i) { return bound[i] >= threshold; },
       [&](uint64_t i, uint64_t o) {
-        for (uint32_t k = 0; k < L; ++k) stypes[o * L + k] = types[i * L + k];
-        for (uint32_t k = 0; k + 1 < L; ++k) swin[o * (L - 1) + k] = win[i * (L - 1) + k];
-        ssigma[o] = sigma[i];
+        if (jx.pre) {
+          // survivor generated from the join index (candidates not materialised)
+          uint32_t l, r;
+          join_pair(jx.loff, jx.nf, jx.pre, jx.lrange, i, l, r);
+          const uint32_t F = jx.F;
+          for (uint32_t k = 0; k < F; ++k) stypes[o * L + k] = jx.ftypes[static_cast<size_t>(l) * F + k];
+          stypes[o * L + F] = jx.ftypes[static_cast<size_t>(r) * F + F - 1];
+          for (uint32_t k = 0; k + 1 < F; ++k) swin[o * (L - 1) + k] = jx.fwin[static_cast<size_t>(l) * (F - 1) + k];
+          const uint32_t rw = jx.fwin[static_cast<size_t>(r) * (F - 1) + F - 2];
+          swin[o * (L - 1) + F - 1] = rw;
+          ssigma[o] = jx.fsigma[l] + (rw >> 16);
+        } else {
+          for (uint32_t k = 0; k < L; ++k) stypes[o * L + k] = types[i * L + k];
+          for (uint32_t k = 0; k + 1 < L; ++k) swin[o * (L - 1) + k] = win[i * (L - 1) + k];
+          ssigma[o] = sigma[i];
+        }
         sidx[o] = static_cast<uint32_t>(i);
       },
       tile_cnt, slot, nullptr);
@@ -594,7 +634,14 @@ struct BoundLaunch {
   uint32_t n_sm;                   // steps used
   uint64_t slice_lo, slice_hi;     // candidates counted here (episode shard)
   unsigned long long* bound;       // [slice_hi - slice_lo], zeroed
+  // join mode (jpre != null, level >= 3, unsharded): candidates are not
+  // materialised; candidate loff[l] + j of left l is left ++ right
+  // jpre[jlrange[2l] + j] (the join index gen_join_kernel would expand)
+  const uint32_t* jpre;
+  const uint32_t* jlrange;
 };
+
+
 
 __device__ __forceinline__ uint32_t dil_rt(uint32_t w, uint32_t h, uint32_t c) {
   return impl::window_any<0, true>(c, h, 0u, w & 0xffffu, w >> 16);
@@ -658,8 +705,16 @@ __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch 
     uint32_t my_tau = ~0u;
     for (uint32_t j = tid; j < mr; j += kBoundThreads) {
       const uint64_t cc = c0 + r0 + j;
-      my_tau = p.ctypes[cc * p.L + p.L - 1];
-      const uint32_t w = p.cwin[cc * (p.L - 1) + p.L - 2];
+      uint32_t w;
+      if (p.jpre) {
+        // candidate = this left ++ right's last node and last constraint
+        const uint32_t rr = p.jpre[p.jlrange[2 * l] + static_cast<uint32_t>(cc - p.loff[l])];
+        my_tau = p.ltypes[static_cast<size_t>(rr) * F + F - 1];
+        w = p.lwin[static_cast<size_t>(rr) * (F - 1) + F - 2];
+      } else {
+        my_tau = p.ctypes[cc * p.L + p.L - 1];
+        w = p.cwin[cc * (p.L - 1) + p.L - 2];
+      }
       uint32_t x = 0;
       for (uint32_t a = 0; a < p.aw.n; ++a)
         if (p.aw.w[a] == w) x = a;
@@ -1086,6 +1141,12 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   b.aw.n = n_alpha;
   b.slice_lo = lf.slice_lo;
   b.slice_hi = lf.slice_lo + n;
+  if (lf.join_mode) {
+    if (lb_tiles(n) > kTcMaxTiles || lf.slice_lo != 0)
+      throw Error(EPI_EUNSUPPORTED, "join-mode pass 1 needs an unsharded level of <= 4M candidates");
+    b.jpre = lf.pre;
+    b.jlrange = lf.lrange;
+  }
   // equal-width alphabet: one shared smear per tile instead of one per window
   uint32_t uw = n_alpha ? (alpha[0] >> 16) - (alpha[0] & 0xffffu) + 1 : 0;
   for (uint32_t a = 0; a < n_alpha; ++a)
@@ -1145,9 +1206,12 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
       uint32_t* tc = scratch_.get<uint32_t>(kMTileCnt, nt);
       prune_count_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(bound, threshold, n, d_counts, tc,
                                                                          d_acc_ + 2);
+      JoinIdx jx{};
+      if (lf.join_mode)
+        jx = JoinIdx{lf.types, lf.win, lf.sigma, lf.pre, lf.lrange, lf.off, static_cast<uint32_t>(lf.nf), L - 1};
       prune_emit_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(bound, threshold, n, L, c.types, c.win,
                                                                         c.sigma, stypes, swin, ssigma, sidx_out,
-                                                                        tc, slot_ptr(mslot));
+                                                                        tc, slot_ptr(mslot), jx);
     } else {
       unsigned long long* lb = scratch_.get<unsigned long long>(kMLookback, nt + 1);
       EPI_CUDA(cudaMemsetAsync(lb, 0, (nt + 1) * sizeof(unsigned long long), st_));
@@ -1538,6 +1602,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
       lefts.types = reinterpret_cast<const uint32_t*>(d_up);
       lefts.win = reinterpret_cast<const uint32_t*>(d_up + o_w);
       lefts.off = reinterpret_cast<const uint64_t*>(d_up + o_o);
+      lefts.pre = reinterpret_cast<const uint32_t*>(d_up + o_p);
+      lefts.lrange = reinterpret_cast<const uint32_t*>(d_up + o_r);
+      lefts.sigma = reinterpret_cast<const uint32_t*>(d_up + o_s);
     }
     DevSet c;
     c.N = L;
@@ -1553,6 +1620,11 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     const bool popbound = cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 && n >= min_pass1() &&
                           amax <= 32 && cfg.n_alpha <= 16 && L <= static_cast<uint32_t>(kBoundMaxL) &&
                           !std::getenv("EPI_PASS1_HULL");
+    // Unsharded popcount levels never materialise their candidates: pass 1
+    // and the survivor gather read them off the join index, and only
+    // survivors can be frequent (compacted from the survivor arrays).
+    lefts.join_mode = popbound && !sharded && level >= 3 && lb_tiles(n) <= kTcMaxTiles &&
+                      !std::getenv("EPI_MATERIALISE");
     // the hull pass 1 synchronises mid-level (its group count): not graphable
     const bool hull_pass1 = level > 1 && !popbound && cfg.mode == EPI_MODE_MINE && cfg.threshold > 1 &&
                             n >= min_pass1();
@@ -1593,7 +1665,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
                                                           d_win, d_sigma, n);
         EPI_CUDA(cudaGetLastError());
         totals.kernel_launches += 1;
-      } else if (level > 2) {
+      } else if (level > 2 && !lefts.join_mode) {
         const unsigned blocks = static_cast<unsigned>((nf * 32 + 255) / 256);
         gen_join_kernel<<<blocks, 256, 0, st_>>>(
             L, reinterpret_cast<const uint32_t*>(d_up), reinterpret_cast<const uint32_t*>(lefts.win),
@@ -1709,6 +1781,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     put(buffers_generation());
     put(compact_cub);
     put(std::getenv("EPI_WALK_SEQ") != nullptr);
+    put(lefts.join_mode);
     const char* fs = std::getenv("EPI_FORCE_SEGMENTS");
     put(fs ? std::strtoull(fs, nullptr, 10) + 1 : 0);
     run_level(key, !sharded && !hull_pass1 && amax <= kMaxHigh, totals, enqueue);
