@@ -115,6 +115,7 @@ void Engine::begin_op() {
   ++stat_epoch_;
   ev_used_ = 0;
   timed_.clear();
+  timed_done_ = 0;
   slot_counters_.clear();
   log_used_ = 0;
   EPI_CUDA(cudaMemsetAsync(d_acc_, 0, 4 * sizeof(unsigned long long), st_));
@@ -142,20 +143,12 @@ void Engine::prefetch_stats() {
   prefetched_epoch_ = stat_epoch_;
 }
 
-void Engine::flush_stats(epi_stats& stats) {
-  const bool ready = prefetched_epoch_ == stat_epoch_;
-  if (!ready) prefetch_stats();
-  char* h = static_cast<char*>(pin_small_.get(64 + kLogSlots * sizeof(uint32_t)));
-  auto* acc = reinterpret_cast<unsigned long long*>(h);
-  auto* log = reinterpret_cast<uint32_t*>(h + 64);
-  // the caller synchronised right after the prefetch when `ready`
-  if (!ready) EPI_CUDA(cudaStreamSynchronize(st_));
-  ++stat_epoch_;
-  stats.patches += acc[0];
-  stats.matched_pairs += acc[1];
-  stats.pruned += acc[2];
-  for (const SlotCounter& s : slot_counters_) *s.target += log[s.slot];
-  for (const Timed& t : timed_) {
+// Resolve timed_[timed_done_, upto) into `stats` (their events are complete
+// and the statistics log holding their live counts is in the pinned mirror).
+void Engine::resolve_timed(epi_stats& stats, size_t upto) {
+  const auto* log = reinterpret_cast<const uint32_t*>(static_cast<const char*>(pin_small_.p) + 64);
+  for (; timed_done_ < upto; ++timed_done_) {
+    const Timed& t = timed_[timed_done_];
     float ms = 0, map_ms = 0;
     EPI_CUDA(cudaEventElapsedTime(&ms, t.e0, t.e1));
     const uint64_t live = t.live_slot >= 0 ? log[t.live_slot] : t.n_host;
@@ -173,7 +166,24 @@ void Engine::flush_stats(epi_stats& stats) {
       stats.tile_steps += live * t.tiles_per_ep;
     }
   }
+}
+
+void Engine::flush_stats(epi_stats& stats) {
+  const bool ready = prefetched_epoch_ == stat_epoch_;
+  if (!ready) prefetch_stats();
+  char* h = static_cast<char*>(pin_small_.get(64 + kLogSlots * sizeof(uint32_t)));
+  auto* acc = reinterpret_cast<unsigned long long*>(h);
+  auto* log = reinterpret_cast<uint32_t*>(h + 64);
+  // the caller synchronised right after the prefetch when `ready`
+  if (!ready) EPI_CUDA(cudaStreamSynchronize(st_));
+  ++stat_epoch_;
+  stats.patches += acc[0];
+  stats.matched_pairs += acc[1];
+  stats.pruned += acc[2];
+  for (const SlotCounter& s : slot_counters_) *s.target += log[s.slot];
+  resolve_timed(stats, timed_.size());
   timed_.clear();
+  timed_done_ = 0;
   slot_counters_.clear();
   log_used_ = 0;
   ev_used_ = 0;  // (begin_op zeroes the device accumulators of the next call)

@@ -178,6 +178,11 @@ class Engine {
   // caller makes anyway; flush_stats then needs no extra round trip when
   // nothing was launched in between.
   void prefetch_stats();
+  // Resolve the timed intervals recorded before index `upto` (their events
+  // complete): the miner does this for level L-1 while level L runs, so the
+  // event-timestamp reads overlap device work instead of trailing the call.
+  void resolve_timed(epi_stats& stats, size_t upto);
+  size_t timed_done_ = 0;
   uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
   const epi_shard* tshard_ = nullptr;  // active time-segment shard (count_device)
   uint64_t iota_n_ = 0;                 // size of the level-1 type-id buffer

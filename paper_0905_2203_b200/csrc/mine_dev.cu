@@ -1784,7 +1784,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     put(lefts.join_mode);
     const char* fs = std::getenv("EPI_FORCE_SEGMENTS");
     put(fs ? std::strtoull(fs, nullptr, 10) + 1 : 0);
+    const size_t timed_before = timed_.size();
     run_level(key, !sharded && !hull_pass1 && amax <= kMaxHigh, totals, enqueue);
+    resolve_timed(totals, timed_before);  // earlier levels', overlapping this one
     EPI_CUDA(cudaStreamSynchronize(st_));
     g_trace.mark("level synced");
     const uint32_t k = *reinterpret_cast<volatile uint32_t*>(h_k);
