@@ -121,17 +121,43 @@ def to_csr(eps):
     return CSR(off, types, lo, hi)
 
 
+_NVML_CHILD = r"""
+import sys, time, pynvml as p
+p.nvmlInit()
+bus = sys.argv[1]
+h = p.nvmlDeviceGetHandleByPciBusId(bus.encode()) if ":" in bus else p.nvmlDeviceGetHandleByIndex(int(bus))
+mx = p.nvmlDeviceGetMaxClockInfo(h, p.NVML_CLOCK_SM)
+out = sys.stdout
+while True:
+    sm = p.nvmlDeviceGetClockInfo(h, p.NVML_CLOCK_SM)
+    r = p.nvmlDeviceGetCurrentClocksEventReasons(h)
+    out.write("%.6f %d %d %d\n" % (time.monotonic(), sm, mx, r))
+    out.flush()
+    time.sleep(0.0005)
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
+
+    NVML in a child process (about one sample per millisecond, CLOCK_MONOTONIC
+    stamps filtered to the region, no GIL contention with the timed loop);
+    nvidia-smi polling when NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits -> names
+    BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+            0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index):
+    def __init__(self, index, bus_id=None):
         self.index = index
+        self.bus_id = bus_id
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._child = None
+        self._span = None
 
     def _run(self):
         while not self._stop.is_set():
@@ -145,25 +171,71 @@ class ClockSampler:
                 pass
             self._stop.wait(0.2)
 
+    def _start_child(self):
+        try:
+            child = subprocess.Popen([sys.executable, "-c", _NVML_CHILD, self.bus_id or str(self.index)],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return None
+        line = child.stdout.readline()  # first sample: NVML works
+        if not line:
+            child.wait(timeout=5)
+            return None
+        self._rows = []
+        self._reader = threading.Thread(target=lambda: self._rows.extend(ln.split() for ln in child.stdout),
+                                        daemon=True)
+        self._reader.start()
+        return child
+
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        self._child = self._start_child()
+        if self._child is None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        self._span = [time.monotonic(), None]
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self._span[1] = time.monotonic()
+        if self._child is not None:
+            time.sleep(0.002)  # a sample past the end of the region
+            self._child.kill()  # the exact child started above
+            self._child.wait(timeout=10)
+            self._reader.join(timeout=10)
+            rows = list(self._rows)
+            t0, t1 = self._span
+            inside = [r for r in rows if len(r) == 4 and t0 <= float(r[0]) <= t1]
+            if not inside:  # region shorter than the sampling period: nearest sample
+                inside = sorted((r for r in rows if len(r) == 4), key=lambda r: abs(float(r[0]) - t1))[:1]
+            self.samples = [("nvml", int(r[1]), int(r[2]), int(r[3])) for r in inside]
+        else:
+            self._stop.set()
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        if self.samples[0][0] == "nvml":
+            sm = [s[1] for s in self.samples]
+            reasons = sorted({n for s in self.samples for b, n in self.BITS.items() if s[3] & b})
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(s[2] for s in self.samples)),
+                    "reasons": reasons, "samples": len(self.samples), "source": "nvml, ~1 ms period"}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples), "source": "nvidia-smi"}
+
+
+def _bus_id(gpu):
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(gpu)
+        return "%08X:%02X:%02X.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+    except Exception:
+        return None
 
 
 def cpu_info():
@@ -325,7 +397,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         step()
     barrier()
-    with ClockSampler(gpu) as clk:
+    with ClockSampler(gpu, _bus_id(gpu)) as clk:
         t_ms, cand_total, stats = timed(step, args.steps)
     clocks = clk.summary()
     step_ms = float(np.sum(t_ms))

@@ -72,7 +72,7 @@ def copy_addr(addr, count: int, dtype) -> np.ndarray:
     if not count:
         return np.zeros(0, dtype=dtype)
     dt = np.dtype(dtype)
-    return np.frombuffer(C.string_at(addr, count * dt.itemsize), dtype=dt).copy()
+    return np.frombuffer((C.c_char * (count * dt.itemsize)).from_address(addr), dtype=dt).copy()
 
 
 class MineResult(C.Structure):
