@@ -215,6 +215,22 @@ epi_status epi_parse_events(const char* text, uint64_t len, uint32_t** types_out
                             int64_t** times_out, uint64_t* n_out, char** names_out,
                             uint32_t* alphabet_out);
 
+/* Binary event files (no reference counterpart): the
+ * stream's SoA as epi_load_stream takes it — a 24-byte header
+ * {"EPIEVT01", u64 n, u32 alphabet, u32 flags = 0}, n u32 types, zero
+ * padding to 8 bytes, n i64 times (little endian). epi_write_events writes
+ * one (no validation; the load validates), epi_read_events returns the
+ * arrays (library-allocated, epi_free), epi_load_stream_file maps the file
+ * and uploads from the mapping through the pinned double-buffered H2D of
+ * epi_load_stream, with the same validation and messages. File errors are
+ * EPI_EDATA ("cannot open event file '<path>'", as load_stream_file,
+ * io.hpp:58-61; "not an event file", "truncated event file"). */
+epi_status epi_write_events(const char* path, const uint32_t* types, const int64_t* times,
+                            uint64_t n, uint32_t alphabet);
+epi_status epi_read_events(const char* path, uint32_t** types_out, int64_t** times_out,
+                           uint64_t* n_out, uint32_t* alphabet_out);
+epi_status epi_load_stream_file(epi_ctx* ctx, const char* path);
+
 /* MEA-culture-shaped bursty generator (no reference
  * counterpart): per-electrode lognormal base rates (base_rate_hz *
  * exp(rate_sigma * N(0,1))), network bursts as a Poisson process at

@@ -94,7 +94,8 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_load_stream_device", "epi_stream_size", "epi_count", "epi_mine", "epi_generate",
            "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
-           "epi_mine_sharded", "epi_count_sharded")
+           "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
+           "epi_load_stream_file")
 
 
 def _load() -> C.CDLL:
@@ -118,6 +119,10 @@ def _load() -> C.CDLL:
                                        C.POINTER(MineResultOut)]),
         "epi_count_sharded": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, C.c_uint32,
                                         C.POINTER(Shard), u64p, u8p, C.POINTER(Stats)]),
+        "epi_write_events": (C.c_int, [C.c_char_p, u32p, i64p, C.c_uint64, C.c_uint32]),
+        "epi_read_events": (C.c_int, [C.c_char_p, C.POINTER(u32p), C.POINTER(i64p), u64p,
+                                      C.POINTER(C.c_uint32)]),
+        "epi_load_stream_file": (C.c_int, [C.c_void_p, C.c_char_p]),
         "epi_parse_events": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(u32p), C.POINTER(i64p), u64p,
                                        C.POINTER(C.c_void_p), C.POINTER(C.c_uint32)]),
         "epi_find_occurrences": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint32,

@@ -21,6 +21,7 @@ std::overflow_error -> OverflowError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Iterable, NamedTuple, Sequence
 
@@ -235,6 +236,12 @@ class Context:
         self._loaded = None
         self._check(N.lib.epi_load_stream(self._h, N.ptr(types, C.c_uint32), N.ptr(times, C.c_int64),
                                           int(types.shape[0]), alphabet))
+
+    def load_file(self, path: str):
+        """Load a binary event file (write_events_binary) straight from its
+        mapping: no parse, pinned double-buffered H2D, from_events validation."""
+        self._loaded = None
+        self._check(N.lib.epi_load_stream_file(self._h, os.fsencode(path)))
 
     def load_device(self, d_types_ptr: int, d_times_ptr: int, n: int, alphabet: int):
         self._loaded = None
@@ -629,3 +636,25 @@ def serialize_stream(stream: EventStream, symbols=None) -> str:
     if len(types) == 0:
         return ""
     return "\n".join(f"{a},{b}" for a, b in zip(names.tolist(), times.tolist())) + "\n"
+
+
+def write_events_binary(path: str, types: np.ndarray, times: np.ndarray, alphabet: int) -> None:
+    """Binary event file (EPIEVT01, include/episodic_b200.h; no reference
+    counterpart): the SoA epi_load_stream takes."""
+    types = np.ascontiguousarray(types, dtype=np.uint32)
+    times = np.ascontiguousarray(times, dtype=np.int64)
+    if types.shape != times.shape:
+        raise InvalidArgument("types and times differ in length")
+    st = N.lib.epi_write_events(os.fsencode(path), N.ptr(types, C.c_uint32), N.ptr(times, C.c_int64),
+                                int(types.shape[0]), int(alphabet))
+    if st != N.EPI_OK:
+        _raise(st, N.lib.epi_last_error(None).decode())
+
+
+def read_events_binary(path: str):
+    """(types, times, alphabet) of a binary event file; DataError on a
+    missing, foreign or truncated file."""
+    tp, tm, n, alpha = N.u32p(), N.i64p(), C.c_uint64(), C.c_uint32()
+    st = N.lib.epi_read_events(os.fsencode(path), C.byref(tp), C.byref(tm), C.byref(n), C.byref(alpha))
+    types, times = _take_stream(st, tp, tm, n)
+    return types, times, int(alpha.value)

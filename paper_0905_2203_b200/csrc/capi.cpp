@@ -1,5 +1,11 @@
 // extern "C" boundary (include/episodic_b200.h). Every entry point catches
 // and maps exceptions to epi_status; messages follow the reference's.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -71,6 +77,55 @@ epi_status guarded(std::string& err, F&& f) {
     return EPI_EINVAL;
   }
 }
+
+// ---- binary event files (EPIEVT01) -----------------------------------------
+// 24-byte header {char magic[8]; u64 n; u32 alphabet; u32 flags = 0}, then
+// the n u32 types, zero padding to 8 bytes, the n i64 times (little endian):
+// the stream's SoA exactly as epi_load_stream takes it, so a load maps the
+// file and uploads straight from the mapping (no parse, no per-event work).
+constexpr char kEvtMagic[8] = {'E', 'P', 'I', 'E', 'V', 'T', '0', '1'};
+constexpr size_t kEvtHeader = 24;
+inline size_t evt_times_off(uint64_t n) { return kEvtHeader + (n * 4 + 7) / 8 * 8; }
+
+struct EventFile {
+  void* base = nullptr;
+  size_t bytes = 0;
+  uint64_t n = 0;
+  uint32_t alphabet = 0;
+  const uint32_t* types = nullptr;
+  const int64_t* times = nullptr;
+  explicit EventFile(const char* path) {
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) throw epi::Error(EPI_EDATA, std::string("cannot open event file '") + path + "'");
+    struct stat sb {};
+    if (::fstat(fd, &sb) != 0 || sb.st_size < static_cast<off_t>(kEvtHeader)) {
+      ::close(fd);
+      throw epi::Error(EPI_EDATA, std::string("not an event file '") + path + "'");
+    }
+    bytes = static_cast<size_t>(sb.st_size);
+    base = ::mmap(nullptr, bytes, PROT_READ, MAP_PRIVATE, fd, 0);
+    ::close(fd);
+    if (base == MAP_FAILED) {
+      base = nullptr;
+      throw epi::Error(EPI_EDATA, std::string("cannot map event file '") + path + "'");
+    }
+    ::madvise(base, bytes, MADV_SEQUENTIAL | MADV_WILLNEED);
+    const char* b = static_cast<const char*>(base);
+    uint32_t flags = 0;
+    std::memcpy(&n, b + 8, 8);
+    std::memcpy(&alphabet, b + 16, 4);
+    std::memcpy(&flags, b + 20, 4);
+    if (std::memcmp(b, kEvtMagic, 8) != 0 || flags != 0)
+      throw epi::Error(EPI_EDATA, std::string("not an event file '") + path + "'");
+    if (n > (bytes - kEvtHeader) / 12 || evt_times_off(n) + n * 8 != bytes)
+      throw epi::Error(EPI_EDATA, std::string("truncated event file '") + path + "'");
+    types = reinterpret_cast<const uint32_t*>(b + kEvtHeader);
+    times = reinterpret_cast<const int64_t*>(b + evt_times_off(n));
+  }
+  ~EventFile() {
+    if (base) ::munmap(base, bytes);
+  }
+};
 
 }  // namespace
 
@@ -288,3 +343,45 @@ epi_status epi_generate_candidates(epi_ctx* ctx, uint64_t level, const epi_episo
 }
 
 }  // extern "C"
+
+epi_status epi_write_events(const char* path, const uint32_t* types, const int64_t* times,
+                            uint64_t n, uint32_t alphabet) {
+  if (!path || (n && (!types || !times))) return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) throw epi::Error(EPI_EDATA, std::string("cannot open event file '") + path + "'");
+    char hdr[kEvtHeader] = {};
+    std::memcpy(hdr, kEvtMagic, 8);
+    std::memcpy(hdr + 8, &n, 8);
+    std::memcpy(hdr + 16, &alphabet, 4);
+    static const char pad[8] = {};
+    const size_t padb = evt_times_off(n) - kEvtHeader - n * 4;
+    const bool ok = std::fwrite(hdr, 1, kEvtHeader, f) == kEvtHeader &&
+                    (n == 0 || std::fwrite(types, 4, n, f) == n) &&
+                    std::fwrite(pad, 1, padb, f) == padb &&
+                    (n == 0 || std::fwrite(times, 8, n, f) == n);
+    if (std::fclose(f) != 0 || !ok)
+      throw epi::Error(EPI_EDATA, std::string("cannot write event file '") + path + "'");
+  });
+}
+
+epi_status epi_read_events(const char* path, uint32_t** types_out, int64_t** times_out,
+                           uint64_t* n_out, uint32_t* alphabet_out) {
+  if (!path || !types_out || !times_out || !n_out || !alphabet_out) return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    EventFile ef(path);
+    std::vector<uint32_t> t(ef.types, ef.types + ef.n);
+    std::vector<int64_t> tm(ef.times, ef.times + ef.n);
+    export_stream(t, tm, types_out, times_out, n_out);
+    *alphabet_out = ef.alphabet;
+  });
+}
+
+epi_status epi_load_stream_file(epi_ctx* ctx, const char* path) {
+  if (!ctx || !path) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    EventFile ef(path);
+    ctx->engine.load_stream_host(ef.types, ef.times, ef.n, ef.alphabet);
+  });
+}

@@ -134,6 +134,29 @@ def test_edge_cases(ctx):
     assert int(got[0]) == 2
 
 
+def test_binary_event_file_load(ctx, tmp_path):
+    """epi_load_stream_file (mapped binary file) == epi_load_stream (arrays):
+    same counts, same validation messages."""
+    from paper_0905_2203_b200 import generate_arrays, GenConfig, write_events_binary
+    types, times = generate_arrays(GenConfig(neurons=12, duration_s=20, base_rate_hz=30, seed=3))
+    rng = np.random.default_rng(1)
+    eps = [([int(x) for x in rng.integers(0, 12, 3)], [(0, 5), (5, 10)]) for _ in range(300)]
+    csr = csr_of(eps)
+    ctx.load_arrays(types, times, 12)
+    want = ctx.count_csr(csr).copy()
+    p = tmp_path / "s.evt"
+    write_events_binary(str(p), types, times, 12)
+    ctx.load_file(str(p))
+    assert np.array_equal(ctx.count_csr(csr), want)
+    for t, tm, a, msg in (([0, 0], [5, 4], 1, "non-decreasing"), ([0, 0], [1, -4], 1, "negative event time"),
+                          ([0, 3], [1, 4], 2, "type id out of range")):
+        write_events_binary(str(p), np.array(t, np.uint32), np.array(tm, np.int64), a)
+        with pytest.raises(DataError, match=msg):
+            ctx.load_file(str(p))
+    with pytest.raises(DataError, match="cannot open event file"):
+        ctx.load_file(str(tmp_path / "missing.evt"))
+
+
 def test_errors(ctx):
     with pytest.raises(DataError, match="non-decreasing"):
         ctx.load_arrays(np.array([0, 0], np.uint32), np.array([5, 4], np.int64), 1)

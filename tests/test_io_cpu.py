@@ -162,3 +162,35 @@ def test_multichunk_file_matches_reference(fault):
     assert len(data) > (1 << 20)
     ok = _compare_with_reference(data)
     assert ok == (fault is None)
+
+
+# ---- binary event files (EPIEVT01; epi_write_events / epi_read_events) -------
+
+def test_binary_event_file_round_trip(tmp_path):
+    from paper_0905_2203_b200 import read_events_binary, write_events_binary
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 2, 3, 1000, 12345):  # odd n exercises the padding before the times
+        types = rng.integers(0, 40, n).astype(np.uint32)
+        times = np.sort(rng.integers(0, 10**12, n)).astype(np.int64)
+        p = tmp_path / f"s{n}.evt"
+        write_events_binary(str(p), types, times, 40)
+        assert p.stat().st_size == 24 + (4 * n + 7) // 8 * 8 + 8 * n
+        t2, tm2, a = read_events_binary(str(p))
+        assert a == 40 and np.array_equal(t2, types) and np.array_equal(tm2, times)
+
+
+def test_binary_event_file_errors(tmp_path):
+    from paper_0905_2203_b200 import read_events_binary, write_events_binary
+    with pytest.raises(DataError, match="cannot open event file"):
+        read_events_binary(str(tmp_path / "missing.evt"))
+    bad = tmp_path / "text.evt"
+    bad.write_bytes(b"A,1\nB,2\nC,3\nD,4\nE,5\nF,6\n")
+    with pytest.raises(DataError, match="not an event file"):
+        read_events_binary(str(bad))
+    p = tmp_path / "cut.evt"
+    write_events_binary(str(p), np.arange(10, dtype=np.uint32), np.arange(10, dtype=np.int64), 10)
+    p.write_bytes(p.read_bytes()[:-1])
+    with pytest.raises(DataError, match="truncated event file"):
+        read_events_binary(str(p))
+    with pytest.raises(DataError, match="cannot open event file"):
+        write_events_binary(str(tmp_path / "no" / "dir.evt"), np.zeros(1, np.uint32), np.zeros(1, np.int64), 1)
