@@ -61,6 +61,7 @@ struct DeviceStream {
   uint64_t raw_cap = 0;
   uint64_t launches = 0;   // kernels launched by loads (stats)
   std::vector<uint64_t> type_hist;  // events per type (a_pad entries), see host_hist
+  uint64_t* h_check = nullptr;      // pinned [2]: validation word, compressed span
   bool hist_on_host = false;
   unsigned long long* d_hist = nullptr;  // events per type on the device (scratch-owned)
   // Host copy of the per-type event counts (one D2H on first use per load).

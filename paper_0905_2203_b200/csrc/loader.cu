@@ -156,6 +156,8 @@ void DeviceStream::release() {
   d_types_raw = nullptr;
   d_times_raw = nullptr;
   raw_cap = 0;
+  if (h_check) cudaFreeHost(h_check);
+  h_check = nullptr;
 }
 
 void DeviceStream::reserve_raw(uint64_t n_events) {
@@ -213,11 +215,13 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
   EPI_CUDA(cudaGetLastError());
   scan_block_sums_kernel<<<1, 1024, 0, st>>>(d_sums, nb);
   EPI_CUDA(cudaGetLastError());
-  unsigned long long h_err = 0;
-  uint64_t h_total = 0;
-  EPI_CUDA(cudaMemcpyAsync(&h_err, d_err, sizeof h_err, cudaMemcpyDeviceToHost, st));
-  EPI_CUDA(cudaMemcpyAsync(&h_total, d_sums + nb, sizeof h_total, cudaMemcpyDeviceToHost, st));
+  // pinned destinations: both copies stay asynchronous, one synchronisation
+  if (!h_check) EPI_CUDA(cudaMallocHost(&h_check, 2 * sizeof(uint64_t)));
+  EPI_CUDA(cudaMemcpyAsync(h_check, d_err, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  EPI_CUDA(cudaMemcpyAsync(h_check + 1, d_sums + nb, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   EPI_CUDA(cudaStreamSynchronize(st));
+  const unsigned long long h_err = h_check[0];
+  const uint64_t h_total = h_check[1];
   launches += 2;
   if (validate && h_err != ~0ull) {
     static const char* kMsg[3] = {"negative event time", "event times must be non-decreasing",
