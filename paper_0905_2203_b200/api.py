@@ -340,9 +340,9 @@ class Context:
             sh = N.Shard(int(rank), int(world), int(min_shard), cb, None)
             self._check(N.lib.epi_mine_sharded(self._h, C.byref(cfg), C.byref(sh), C.byref(res)))
         nl = int(res.n_levels)
-        cands = N.copy_addr(res.level_candidates, nl, np.uint64).tolist()
-        offs = N.copy_addr(res.level_offsets, nl + 1, np.uint64).tolist()
-        ms = N.copy_addr(res.level_ms, nl, np.float64).tolist()
+        cands = (C.c_uint64 * nl).from_address(res.level_candidates)[:] if nl else []
+        offs = (C.c_uint64 * (nl + 1)).from_address(res.level_offsets)[:] if res.level_offsets else [0]
+        ms = (C.c_double * nl).from_address(res.level_ms)[:] if nl else []
         fr = res.frequent
         nf = int(fr.n_episodes)
         if nf:
