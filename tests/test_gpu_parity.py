@@ -447,6 +447,25 @@ def test_mine_wide_windows_vs_reference(ctx, seed, monkeypatch):
         assert write_mining_csv(r) == csv_ref, (seed, mode)
 
 
+def test_mine_stats_stable_across_graph_replays(ctx, monkeypatch):
+    """The statistics a mining call reports (device counters resolved from the
+    log, event timings resolved while the next level runs) are the same for a
+    direct run, the captured run and graph replays."""
+    types, times = generate_arrays(_gen("cfg2"))
+    ctx.load_arrays(types, times, 26)
+    keys = ("episodes", "pass1_groups", "pass2_episodes", "pruned", "segments", "patches",
+            "episode_events", "tile_steps", "bound_words")
+    monkeypatch.setenv("EPI_NO_GRAPH", "1")
+    want = ctx.mine_raw(250, BINS, 4, MODE_MINE)[5]
+    monkeypatch.delenv("EPI_NO_GRAPH")
+    for it in range(4):
+        st = ctx.mine_raw(250, BINS, 4, MODE_MINE)[5]
+        assert {k: st[k] for k in keys} == {k: want[k] for k in keys}, it
+        assert st["bound_ms"] > 0 and st["pass2_ms"] > 0, it
+        assert abs(st["pass1_ms"] + st["pass2_ms"] - st["total_ms"]) < 1e-3, it
+        assert st["map_ms"] + st["concat_ms"] <= st["pass2_ms"] + 1e-3, it
+
+
 def test_mine_graph_replay(ctx, golden_configs, monkeypatch):
     """Per-level CUDA graphs: repeated mining of cfg2 (first run direct,
     second captured, then replayed) and, interleaved, of a type-relabelled
