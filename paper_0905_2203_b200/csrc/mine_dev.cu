@@ -459,6 +459,24 @@ __global__ void __launch_bounds__(kLbThreads) surv_emit_tc(const uint64_t* __res
       tile_cnt, slot, host_k);
 }
 
+// Same, one CTA: the survivors are few whenever pass 1 pays, and when they
+// are many pass 2 on them dwarfs a single-CTA pass over them.
+__global__ void __launch_bounds__(kOneBlk) surv_compact_1blk(const uint64_t* __restrict__ counts,
+                                                             uint64_t threshold, const uint32_t* __restrict__ m_dev,
+                                                             uint32_t L, const uint32_t* __restrict__ types,
+                                                             const uint32_t* __restrict__ win, uint32_t* otypes,
+                                                             uint32_t* owin, uint64_t* ocounts, uint32_t* slot,
+                                                             uint32_t* host_k) {
+  one_block_compact(
+      *m_dev, [&](uint64_t i) { return counts[i] >= threshold; },
+      [&](uint64_t i, uint32_t o) {
+        for (uint32_t k = 0; k < L; ++k) otypes[static_cast<size_t>(o) * L + k] = types[i * L + k];
+        for (uint32_t k = 0; k + 1 < L; ++k) owin[static_cast<size_t>(o) * (L - 1) + k] = win[i * (L - 1) + k];
+        ocounts[o] = counts[i];
+      },
+      slot, host_k);
+}
+
 __global__ void __launch_bounds__(kLbThreads) prune_count_tc(const unsigned long long* __restrict__ bound,
                                                              uint64_t threshold, uint64_t n, uint64_t* counts,
                                                              uint32_t* tile_cnt, unsigned long long* pruned) {
@@ -1699,8 +1717,15 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         counts_all = d_all;
       }
       // threshold + compaction in candidate order, straight to host memory
-      if (surv.slot >= 0) {
+      if (surv.slot >= 0 && !std::getenv("EPI_SURV_TC")) {
         // only pass-1 survivors can be frequent: compact those (in order)
+        surv_compact_1blk<<<1, kOneBlk, 0, st_>>>(
+            surv.counts, cfg.threshold, slot_ptr(surv.slot), L, surv.types, surv.win,
+            reinterpret_cast<uint32_t*>(dm + o_ft), reinterpret_cast<uint32_t*>(dm + o_fw),
+            reinterpret_cast<uint64_t*>(dm + o_fc), slot_ptr(new_slot()), h_k);
+        EPI_CUDA(cudaGetLastError());
+        totals.kernel_launches += 1;
+      } else if (surv.slot >= 0) {
         const uint64_t nt = std::max<uint64_t>(lb_tiles(n), 1);
         uint32_t* tc = scratch_.get<uint32_t>(kMTileCnt, nt);
         surv_count_tc<<<static_cast<unsigned>(nt), kLbThreads, 0, st_>>>(surv.counts, cfg.threshold,
@@ -1781,6 +1806,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
     put(buffers_generation());
     put(compact_cub);
     put(std::getenv("EPI_WALK_SEQ") != nullptr);
+    put(std::getenv("EPI_SURV_TC") != nullptr);
     put(lefts.join_mode);
     const char* fs = std::getenv("EPI_FORCE_SEGMENTS");
     put(fs ? std::strtoull(fs, nullptr, 10) + 1 : 0);

@@ -224,11 +224,12 @@ def test_cfg1_all_pairs(ctx, golden_configs):
 
 @pytest.mark.parametrize("mode,knob", [(MODE_MINE, None), (MODE_EXACT, None), (MODE_MINE, "EPI_COMPACT_CUB"),
                                        (MODE_MINE, "EPI_PASS1_HULL"), (MODE_MINE, "EPI_WALK_SEQ"),
-                                       (MODE_MINE, "EPI_MATERIALISE")])
+                                       (MODE_MINE, "EPI_MATERIALISE"), (MODE_MINE, "EPI_SURV_TC")])
 def test_cfg2_mining(ctx, golden_configs, mode, knob, monkeypatch):
     """cfg2 mining CSV == the reference's, on the default device path and on
     each alternative it keeps (CUB multi-kernel compaction, hull pass 1,
-    sequential concat walk, materialised candidates)."""
+    sequential concat walk, materialised candidates, multi-CTA survivor
+    compaction)."""
     from paper_0905_2203_b200 import MiningConfig, mine, write_mining_csv, EventStream
     if knob:
         monkeypatch.setenv(knob, "1")
