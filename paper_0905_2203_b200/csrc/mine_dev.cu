@@ -651,7 +651,8 @@ struct BoundLaunch {
   uint32_t sm[5];                  // doubling-smear shifts covering uniform_w
   uint32_t n_sm;                   // steps used
   uint64_t slice_lo, slice_hi;     // candidates counted here (episode shard)
-  unsigned long long* bound;       // [slice_hi - slice_lo], zeroed
+  unsigned long long* bound;       // [slice_hi - slice_lo], zeroed unless direct
+  bool direct;                     // one time split: every candidate stored once
   // join mode (jpre != null, level >= 3, unsharded): candidates are not
   // materialised; candidate loff[l] + j of left l is left ++ right
   // jpre[jlrange[2l] + j] (the join index gen_join_kernel would expand)
@@ -887,7 +888,13 @@ __global__ void __launch_bounds__(kBoundThreads) bound_kernel(const BoundLaunch 
       s_acc[j][lane] = 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && v) atomicAdd(p.bound + (c0 - p.slice_lo) + r0 + j, static_cast<unsigned long long>(v));
+      if (lane == 0) {
+        unsigned long long* dst = p.bound + (c0 - p.slice_lo) + r0 + j;
+        if (p.direct)
+          *dst = v;
+        else if (v)
+          atomicAdd(dst, static_cast<unsigned long long>(v));
+      }
     }
   }
 }
@@ -1143,7 +1150,6 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
   stats.episodes += n;
   stats.pass1_groups += n;
   unsigned long long* bound = scratch_.get<unsigned long long>(kMBound, n);
-  EPI_CUDA(cudaMemsetAsync(bound, 0, n * sizeof(unsigned long long), st_));
   BoundLaunch b{};
   b.occ = stream_.d_occ;
   b.blk_words = stream_.blk_words;
@@ -1189,6 +1195,9 @@ void Engine::count_device_popbound(const DevSet& c, const PopLefts& lf, uint64_t
                                              std::max<int64_t>(chunks, 1));
   b.span = static_cast<int32_t>((chunks + splits - 1) / splits * kBoundThreads);
   const int64_t ysplits = (static_cast<int64_t>(stream_.n_tiles) + b.span - 1) / b.span;
+  // one CTA per left covers each candidate once: store, no zeroing pass
+  b.direct = ysplits <= 1;
+  if (!b.direct) EPI_CUDA(cudaMemsetAsync(bound, 0, n * sizeof(unsigned long long), st_));
   Timed t{next_event(), nullptr, next_event(), &stats.pass1_ms, -1, n, 0, false};
   t.e_map = t.e1;
   t.ms_out2 = &stats.bound_ms;
