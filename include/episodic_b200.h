@@ -243,6 +243,14 @@ epi_status epi_generate_bursty(uint32_t electrodes, double duration_s, double ba
                                const epi_episode_batch* embedded, const double* rates,
                                uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
 
+/* Seeded synthetic candidate episodes for the bench configs (no reference
+ * counterpart; the draw order of SURVEY §8d config 3): one std::mt19937_64
+ * stream seeded with `seed`; per episode `nodes` types (raw output %
+ * alphabet) then nodes-1 constraint-bin indices (raw output % n_bins).
+ * types_out holds count*nodes entries, bins_out count*(nodes-1). */
+epi_status epi_random_episodes(uint64_t seed, uint64_t count, uint32_t nodes, uint32_t alphabet,
+                               uint32_t n_bins, uint32_t* types_out, uint32_t* bins_out);
+
 /* generate_candidates (miner.hpp:76-109) exposed for parity tests and for
  * callers that drive their own level loop: `frequent` holds level-1 frequent
  * episodes (all of length level-1; ignored for level 1). Host-only (no device

@@ -238,3 +238,51 @@ class RefDataError(RuntimeError):
 
 def ref_default_workers() -> int:
     return int(ref().ref_default_workers())
+
+
+def ref_generate(neurons, duration_s, base_rate_hz, seed, embedded=()):
+    """generate() of the reference (E/datagen.hpp:71-122) -> (types u32,
+    times i64). `embedded`: [(types, [(lo, hi), ...], rate_hz), ...]."""
+    lib = ref()
+    off = _u32(np.cumsum([0] + [len(t) for t, _, _ in embedded]))
+    et = _u32([x for t, _, _ in embedded for x in t] or [0])
+    lo = _i64([c[0] for _, cs, _ in embedded for c in cs] or [0])
+    hi = _i64([c[1] for _, cs, _ in embedded for c in cs] or [0])
+    rates = np.ascontiguousarray([r for _, _, r in embedded] or [0.0], dtype=np.float64)
+    tp, tm, n = u32p(), i64p(), C.c_uint64()
+    st = lib.ref_generate(int(neurons), float(duration_s), float(base_rate_hz), int(seed) & U64_MAX,
+                          _p(off, C.c_uint32), _p(et, C.c_uint32), _p(lo, C.c_int64), _p(hi, C.c_int64),
+                          _p(rates, C.c_double), len(embedded), C.byref(tp), C.byref(tm), C.byref(n))
+    if st != 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    k = int(n.value)
+    types = np.ctypeslib.as_array(tp, shape=(max(k, 1),))[:k].copy()
+    times = np.ctypeslib.as_array(tm, shape=(max(k, 1),))[:k].copy()
+    lib.ref_free(C.cast(tp, C.c_void_p))
+    lib.ref_free(C.cast(tm, C.c_void_p))
+    return types, times
+
+
+def mt_episodes(seed, count, nodes, alphabet, bins):
+    """Seeded synthetic candidates in the bench's draw order (one
+    std::mt19937_64 stream: per episode `nodes` types % alphabet, then nodes-1
+    bin indices % len(bins)); pure Python, for small counts."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(_HERE), "tests"))
+    from instances import MT19937_64
+    g = MT19937_64(seed)
+    out = []
+    for _ in range(count):
+        t = [g() % alphabet for _ in range(nodes)]
+        b = [bins[g() % len(bins)] for _ in range(nodes - 1)]
+        out.append((t, b))
+    return out
+
+
+def csr_arrays(episodes):
+    """[(types, [(lo, hi)])] -> (offsets u32, types u32, low i64, high i64)."""
+    off = _u32(np.cumsum([0] + [len(t) for t, _ in episodes]))
+    et = _u32([x for t, _ in episodes for x in t])
+    lo = _i64([c[0] for _, cs in episodes for c in cs])
+    hi = _i64([c[1] for _, cs in episodes for c in cs])
+    return off, et, lo, hi

@@ -95,7 +95,7 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
            "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
-           "epi_load_stream_file")
+           "epi_load_stream_file", "epi_random_episodes")
 
 
 def _load() -> C.CDLL:
@@ -139,6 +139,8 @@ def _load() -> C.CDLL:
                                           C.POINTER(i64p), u64p]),
         "epi_generate_candidates": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(EpisodeBatch), i64p, i64p,
                                               C.c_uint64, C.c_uint32, C.POINTER(EpisodeBatch)]),
+        "epi_random_episodes": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          u32p, u32p]),
         "epi_version": (C.c_char_p, []),
         "epi_probe_int32": (C.c_int, [C.c_int, C.c_int, f64p]),
     }

@@ -583,6 +583,23 @@ def generate_bursty_arrays(cfg: BurstConfig):
     return _take_stream(st, tp, tm, n)
 
 
+def random_episodes_csr(seed: int, count: int, nodes: int, alphabet: int, bins) -> N.CSR:
+    """Seeded synthetic candidates (epi_random_episodes: one mt19937_64
+    stream, per episode `nodes` types % alphabet then nodes-1 indices into
+    `bins`), as a CSR batch."""
+    types = np.zeros(count * nodes, dtype=np.uint32)
+    bidx = np.zeros(max(count * (nodes - 1), 1), dtype=np.uint32)
+    st = N.lib.epi_random_episodes(int(seed) & ((1 << 64) - 1), int(count), int(nodes), int(alphabet),
+                                   len(bins), N.ptr(types, C.c_uint32), N.ptr(bidx, C.c_uint32))
+    if st != 0:
+        _raise(st, N.lib.epi_last_error(None).decode())
+    bidx = bidx[:count * (nodes - 1)]
+    lo = np.array([b[0] for b in bins], np.int64)[bidx]
+    hi = np.array([b[1] for b in bins], np.int64)[bidx]
+    off = (np.arange(count + 1, dtype=np.uint64) * nodes).astype(np.uint32)
+    return N.CSR(off, types, lo, hi)
+
+
 def generate(cfg: GenConfig) -> EventStream:
     types, times = generate_arrays(cfg)
     return EventStream(types, times, cfg.neurons)

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <random>
 #include <new>
 #include <string>
 #include <vector>
@@ -115,10 +116,14 @@ struct EventFile {
     std::memcpy(&n, b + 8, 8);
     std::memcpy(&alphabet, b + 16, 4);
     std::memcpy(&flags, b + 20, 4);
-    if (std::memcmp(b, kEvtMagic, 8) != 0 || flags != 0)
-      throw epi::Error(EPI_EDATA, std::string("not an event file '") + path + "'");
-    if (n > (bytes - kEvtHeader) / 12 || evt_times_off(n) + n * 8 != bytes)
-      throw epi::Error(EPI_EDATA, std::string("truncated event file '") + path + "'");
+    // the destructor does not run for a throwing constructor: unmap first
+    auto reject = [&](const char* what) {
+      ::munmap(base, bytes);
+      base = nullptr;
+      throw epi::Error(EPI_EDATA, std::string(what) + " '" + path + "'");
+    };
+    if (std::memcmp(b, kEvtMagic, 8) != 0 || flags != 0) reject("not an event file");
+    if (n > (bytes - kEvtHeader) / 12 || evt_times_off(n) + n * 8 != bytes) reject("truncated event file");
     types = reinterpret_cast<const uint32_t*>(b + kEvtHeader);
     times = reinterpret_cast<const int64_t*>(b + evt_times_off(n));
   }
@@ -297,6 +302,24 @@ epi_status epi_generate_bursty(uint32_t electrodes, double duration_s, double ba
     epi::generate_bursty(electrodes, duration_s, base_rate_hz, rate_sigma, burst_rate_hz,
                          burst_min_ms, burst_max_ms, burst_gain, seed, embedded, rates, t, tm);
     export_stream(t, tm, types_out, times_out, n_out);
+  });
+}
+
+epi_status epi_random_episodes(uint64_t seed, uint64_t count, uint32_t nodes, uint32_t alphabet,
+                               uint32_t n_bins, uint32_t* types_out, uint32_t* bins_out) {
+  if ((count && !types_out) || (count && nodes > 1 && !bins_out)) return EPI_EINVAL;
+  return guarded(g_free_err, [&] {
+    if (nodes < 1 || alphabet < 1 || (nodes > 1 && n_bins < 1))
+      throw epi::Error(EPI_EINVAL, "random_episodes: need nodes >= 1, alphabet >= 1, n_bins >= 1");
+    // one sequential std::mt19937_64 stream (the reference's Rng engine,
+    // E/datagen.hpp:44-62): per episode `nodes` type draws, then nodes-1 bin
+    // draws, each raw output modulo the range
+    std::mt19937_64 g(seed);
+    for (uint64_t e = 0; e < count; ++e) {
+      for (uint32_t k = 0; k < nodes; ++k) types_out[e * nodes + k] = static_cast<uint32_t>(g() % alphabet);
+      for (uint32_t k = 0; k + 1 < nodes; ++k)
+        bins_out[e * (nodes - 1) + k] = static_cast<uint32_t>(g() % n_bins);
+    }
   });
 }
 

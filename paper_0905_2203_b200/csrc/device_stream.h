@@ -47,6 +47,7 @@ class DeviceScratch {
 
 struct DeviceStream {
   uint64_t n = 0;          // events
+  bool valid = false;      // set only once a load (validation + bitmap build) succeeded
   uint32_t alphabet = 0;   // event-type alphabet size
   uint32_t a_pad = 4;      // words per tile row (alphabet + 1 spare, rounded up to 4)
   uint64_t n_tiles = 0;    // 32 ms tiles covering the compressed span

@@ -111,6 +111,10 @@ uint64_t Engine::buffers_generation() const {
          (map_small_.generation << 33);
 }
 
+void Engine::require_stream() const {
+  if (!stream_.valid) throw Error(EPI_EINVAL, "no event stream loaded (epi_load_stream first)");
+}
+
 void Engine::begin_op() {
   ++stat_epoch_;
   ev_used_ = 0;
@@ -630,6 +634,7 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
   epi_stats stats{};
   const uint64_t n = b.n_episodes;
   if (n && (!b.offsets || !counts_out)) throw Error(EPI_EINVAL, "epi_count: null batch arrays");
+  require_stream();
   begin_op();
   if (mode > EPI_MODE_MINE) throw Error(EPI_EINVAL, "epi_count: unknown mode");
   // validate(Episode) for every candidate first (E/types.hpp:87-92).
@@ -676,6 +681,7 @@ void Engine::count_batch_sharded(const epi_episode_batch& b, uint64_t threshold,
   const uint64_t W = shard.world, R = shard.rank;
   if (W == 0 || R >= W || (W > 1 && !shard.allgather))
     throw Error(EPI_EINVAL, "count: invalid shard (rank, world, allgather)");
+  require_stream();
   if (W == 1) {
     count_batch(b, threshold, mode, counts_out, frequent_out, stats_out);
     return;

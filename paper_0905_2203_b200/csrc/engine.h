@@ -94,6 +94,8 @@ class Engine {
   void load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,
                           uint32_t alphabet);
   uint64_t stream_size() const { return stream_.n; }
+  // EPI_EINVAL unless a stream load succeeded (counting needs the bitmap)
+  void require_stream() const;
   uint64_t last_load_h2d = 0;
   uint32_t alphabet() const { return stream_.alphabet; }
 

@@ -174,6 +174,9 @@ void DeviceStream::reserve_raw(uint64_t n_events) {
 
 void DeviceStream::load(uint64_t n_events, uint32_t alphabet_size, cudaStream_t st,
                         DeviceScratch& scratch) {
+  // a failed load leaves no half-updated stream behind: counting refuses to
+  // run until a later load succeeds
+  valid = false;
   n = 0;
   alphabet = alphabet_size;
   // One spare always-zero column (index `alphabet`) for episode types that
@@ -202,6 +205,7 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
     EPI_CUDA(cudaMemsetAsync(d_hist, 0, a_pad * sizeof(unsigned long long), st));
     n = 0;
     span = 0;
+    valid = true;
     return;
   }
   const uint32_t* d_types = d_types_raw;
@@ -243,6 +247,7 @@ void DeviceStream::build(uint64_t n_events, uint32_t cap, bool validate, cudaStr
   n = n_events;
   n_tiles = tiles;
   span = h_total + 1;
+  valid = true;
 }
 
 const std::vector<uint64_t>& DeviceStream::host_hist(cudaStream_t st) {

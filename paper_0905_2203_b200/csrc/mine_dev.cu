@@ -225,14 +225,30 @@ __device__ __forceinline__ void one_block_compact(uint64_t n, Pred&& pred, Emit&
                                                   uint32_t* host_total) {
   using BS = cub::BlockScan<uint32_t, kOneBlk>;
   __shared__ typename BS::TempStorage ts;
-  const uint64_t chunk = (n + kOneBlk - 1) / kOneBlk;
-  const uint64_t b = min(n, threadIdx.x * chunk), e = min(n, b + chunk);
-  uint32_t cnt = 0;
-  for (uint64_t i = b; i < e; ++i) cnt += pred(i) ? 1u : 0u;
-  uint32_t off = 0, total = 0;
-  BS(ts).ExclusiveSum(cnt, off, total);
-  for (uint64_t i = b; i < e; ++i)
-    if (pred(i)) emit(i, off++);
+  uint32_t total = 0;
+  if (n <= kOneBlkMax) {
+    // small: one contiguous chunk per thread, one scan
+    const uint64_t chunk = (n + kOneBlk - 1) / kOneBlk;
+    const uint64_t b = min(n, threadIdx.x * chunk), e = min(n, b + chunk);
+    uint32_t cnt = 0;
+    for (uint64_t i = b; i < e; ++i) cnt += pred(i) ? 1u : 0u;
+    uint32_t off = 0;
+    BS(ts).ExclusiveSum(cnt, off, total);
+    for (uint64_t i = b; i < e; ++i)
+      if (pred(i)) emit(i, off++);
+  } else {
+    // large (a device-sized count beyond the small-launch regime): coalesced
+    // rounds of kOneBlk items, one block scan each, running offset
+    for (uint64_t base = 0; base < n; base += kOneBlk) {
+      const uint64_t i = base + threadIdx.x;
+      const bool f = i < n && pred(i);
+      uint32_t off = 0, agg = 0;
+      BS(ts).ExclusiveSum(f ? 1u : 0u, off, agg);
+      if (f) emit(i, total + off);
+      total += agg;
+      __syncthreads();  // TempStorage reuse
+    }
+  }
   if (threadIdx.x == 0) {
     *total_slot = total;
     if (host_total) *reinterpret_cast<volatile uint32_t*>(host_total) = total;
@@ -1401,6 +1417,7 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
   const uint32_t W = shard ? shard->world : 1, R = shard ? shard->rank : 0;
   if (shard && (W == 0 || R >= W || (W > 1 && !shard->allgather)))
     throw Error(EPI_EINVAL, "mine: invalid shard (rank, world, allgather)");
+  require_stream();
   std::vector<uint32_t> awin(cfg.n_alpha), ahi(cfg.n_alpha);
   int64_t amax = 0, amin_lo = INT64_MAX;
   int awidth = -1;

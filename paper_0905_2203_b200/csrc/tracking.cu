@@ -291,6 +291,7 @@ void Engine::track_batch(const epi_episode_batch& b, uint32_t direction, uint64_
   const uint64_t n = b.n_episodes;
   if (n && (!b.offsets || (!counts_out && !off_out)))
     throw Error(EPI_EINVAL, "epi_track: null batch arrays");
+  require_stream();
   for (uint64_t e = 0; e < n; ++e) {
     if (b.offsets[e + 1] < b.offsets[e]) throw Error(EPI_EINVAL, "epi_track: offsets not monotone");
     const uint32_t N = b.offsets[e + 1] - b.offsets[e];
