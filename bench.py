@@ -1,26 +1,28 @@
 """Benchmark: episode-events counted per second on B200 (BASELINE.json metric).
 
-Default workload = BASELINE.json configs[1] ("cfg2"): Sym26 synthetic spike
-train (26 neurons, 60 s, 32 Hz, seed 1, four embedded 4-node chains at 5 Hz:
-54,750 events), level-wise mining to 4-node episodes over the constraint
-alphabet {(0,5],(5,10],(10,15]} at threshold 250 with two-pass elimination.
-One step = one full mine() (levels 1-4: 26 + 2,028 + 142,228 + 4
-candidates). Work unit = (candidate episode, stream event) pair, counted for
-every generated candidate, pruned or not (the reference counts them all).
+Default workload = the BASELINE.json metric's own configuration, configs[4]
+("cfg5", the candidate-count sweep) at its largest single-GPU candidate set:
+a 10M-event synthetic spike train (64 neurons at 20 Hz, the reference's
+generate(), seed 5 + n) and 1,000,000 seeded random 3-node candidates over
+the constraint bins {(0,5],(5,10],(10,15]} (one mt19937_64(55) stream: three
+types % 64 then two bin indices % 3 per candidate), exact counts of every
+candidate. One step = one epi_count of the whole candidate set. Work unit =
+(candidate episode, stream event) pair.
 
-  value  device-resident: stream already in HBM, step = epi_mine on it,
-         timed with CUDA events (synchronous call; host candidate generation
-         is inside the step).
+  value  device-resident: stream already in HBM, step = epi_count of the
+         candidates (host batch in, host counts out), timed with CUDA events.
   e2e    through the public C-ABI from pinned host buffers: epi_load_stream
-         (12 B/event H2D + device validation/bitmap build) + epi_mine (which
-         returns counts to the host) every step.
+         (12 B/event H2D + device validation/bitmap build) + epi_count every
+         step.
 
---config cfg1|cfg3|cfg4|cfg5 selects the other single-GPU configs (exact
-counting only): cfg4 = MEA-shaped bursty stream (60 electrodes, ~100M
-events) x 10,002 5-node candidates; cfg5 = one cell of the sweep
-(--cfg5-events, --cfg5-cands: 64 types at 20 Hz, random 3-node candidates).
---impl reference times the reference's own CPU implementation (oracle/_ref,
-compiled from /root/reference) on the host cores instead.
+--config cfg1|cfg2|cfg3|cfg4 and --cfg5-events/--cfg5-cands select the other
+configs: cfg2 = Sym26 level-wise mining to level 4 with two-pass elimination;
+cfg4 = MEA-shaped bursty stream (60 electrodes, ~100M events) x 10,002 5-node
+candidates.
+--impl reference times the reference's own CPU implementation (oracle/_ref =
+the unmodified reference headers compiled in place) on the host cores: its
+generate() for the stream, its count_tracking episode-parallel over a seeded
+candidate subset (cfg2: its full mine()); nothing of this package is loaded.
 """
 from __future__ import annotations
 
@@ -40,76 +42,75 @@ sys.path.insert(0, ROOT)
 BINS = [(0, 5), (5, 10), (10, 15)]
 
 
-def make_config(name):
-    from paper_0905_2203_b200 import Embedding, Episode, GenConfig
-    if name in ("cfg1",):
-        return GenConfig(26, 60, 32, [Embedding(Episode([0, 1, 2, 3], [(5, 10)] * 3), 2.0)], 1)
+CFG2_CHAINS = [([0, 1, 2, 3], [BINS[1]] * 3), ([4, 5, 6, 7], [BINS[0], BINS[1], BINS[2]]),
+               ([8, 9, 10, 11], [BINS[2], BINS[0], BINS[1]]), ([12, 13, 14, 15], [BINS[1], BINS[2], BINS[0]])]
+CFG4_CHAINS = [([0, 7, 13, 21, 33], [(5, 10), (0, 5), (10, 15), (5, 10)]), ([40, 41, 42, 43, 44], [(0, 5)] * 4)]
+# seeded candidate sequences (mt19937_64(seed): per candidate `nodes` types %
+# alphabet, then nodes-1 bin indices % 3): (seed, nodes, alphabet)
+CAND_SEQ = {"cfg3": (5, 3, 64), "cfg4": (44, 5, 60), "cfg5": (55, 3, 64)}
+
+
+def stream_spec(name, cfg5_events=10_000_000):
+    """Generator parameters of a config's stream."""
+    if name == "cfg1":
+        return {"kind": "generate", "neurons": 26, "duration_s": 60, "rate_hz": 32, "seed": 1,
+                "embedded": [([0, 1, 2, 3], [(5, 10)] * 3, 2.0)]}
     if name == "cfg2":
-        eps = [([0, 1, 2, 3], [BINS[1]] * 3), ([4, 5, 6, 7], [BINS[0], BINS[1], BINS[2]]),
-               ([8, 9, 10, 11], [BINS[2], BINS[0], BINS[1]]),
-               ([12, 13, 14, 15], [BINS[1], BINS[2], BINS[0]])]
-        return GenConfig(26, 60, 32, [Embedding(Episode(t, c), 5.0) for t, c in eps], 1)
+        return {"kind": "generate", "neurons": 26, "duration_s": 60, "rate_hz": 32, "seed": 1,
+                "embedded": [(t, c, 5.0) for t, c in CFG2_CHAINS]}
     if name == "cfg3":
-        return GenConfig(64, 7813, 20, [], 3)
+        return {"kind": "generate", "neurons": 64, "duration_s": 7813, "rate_hz": 20, "seed": 3, "embedded": []}
+    if name == "cfg4":
+        # MEA-culture-shaped: 60 electrodes, lognormal rates, network bursts,
+        # two embedded 5-node chains; ~100M events (no reference counterpart)
+        return {"kind": "bursty", "electrodes": 60, "duration_s": 175_000, "seed": 4,
+                "embedded": [(t, c, 0.5) for t, c in CFG4_CHAINS]}
+    if name == "cfg5":
+        return {"kind": "generate", "neurons": 64, "duration_s": cfg5_events / (64 * 20), "rate_hz": 20,
+                "seed": 5 + cfg5_events, "embedded": []}
     raise SystemExit(f"unknown config {name}")
 
 
+def alphabet_of(spec):
+    return spec["neurons"] if spec["kind"] == "generate" else spec["electrodes"]
+
+
 def make_stream(name, cfg5_events=10_000_000):
-    """(types, times, alphabet) of a bench config; synthetic, seeded."""
+    """(types, times, alphabet) of a config, from this package's generators
+    (bit-exact restatement of the reference's generate())."""
     from paper_0905_2203_b200 import (BurstConfig, Embedding, Episode, GenConfig, generate_arrays,
                                       generate_bursty_arrays)
-    if name == "cfg4":
-        # MEA-culture-shaped (SURVEY 8d config 4): 60 electrodes, lognormal
-        # rates, network bursts, two embedded 5-node chains; ~100M events
-        t, tm = generate_bursty_arrays(BurstConfig(electrodes=60, duration_s=175_000, seed=4,
-                                                   embedded=[Embedding(c, 0.5) for c in CFG4_CHAINS()]))
-        return t, tm, 60
-    if name == "cfg5":
-        t, tm = generate_arrays(GenConfig(64, cfg5_events / (64 * 20), 20, [], 5 + cfg5_events))
-        return t, tm, 64
-    t, tm = generate_arrays(make_config(name))
-    return t, tm, 64 if name == "cfg3" else 26
-
-
-def CFG4_CHAINS():
-    from paper_0905_2203_b200 import Episode
-    return [Episode([0, 7, 13, 21, 33], [(5, 10), (0, 5), (10, 15), (5, 10)]),
-            Episode([40, 41, 42, 43, 44], [(0, 5)] * 4)]
-
-
-def random_candidates(seed, count, alphabet, nodes):
-    rng = np.random.default_rng(seed)
-    return [([int(x) for x in rng.integers(0, alphabet, nodes)],
-             [BINS[int(b)] for b in rng.integers(0, 3, nodes - 1)]) for _ in range(count)]
-
-
-def count_candidates(name, cfg5_cands=10000):
-    if name == "cfg1":
-        return cfg1_candidates()
-    if name == "cfg3":
-        return cfg3_candidates()
-    if name == "cfg4":
-        return random_candidates(44, 10000, 60, 5) + [(c.types, c.constraints) for c in CFG4_CHAINS()]
-    if name == "cfg5":
-        return random_candidates(55, cfg5_cands, 64, 3)
-    raise SystemExit(f"{name} is not a counting config")
+    sp = stream_spec(name, cfg5_events)
+    emb = [Embedding(Episode(t, c), r) for t, c, r in sp["embedded"]]
+    if sp["kind"] == "bursty":
+        t, tm = generate_bursty_arrays(BurstConfig(electrodes=sp["electrodes"], duration_s=sp["duration_s"],
+                                                   seed=sp["seed"], embedded=emb))
+    else:
+        t, tm = generate_arrays(GenConfig(sp["neurons"], sp["duration_s"], sp["rate_hz"], emb, sp["seed"]))
+    return t, tm, alphabet_of(sp)
 
 
 def cfg1_candidates():
     return [([a, b], [(5, 10)]) for a in range(26) for b in range(26)]
 
 
-def cfg3_candidates(count=10000):
-    """mt19937_64(5): t0,t1,t2 = rng()%64 then b0,b1 = rng()%3."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from instances import MT19937_64
-    g = MT19937_64(5)
-    out = []
-    for _ in range(count):
-        t = [g() % 64 for _ in range(3)]
-        b = [BINS[g() % 3] for _ in range(2)]
-        out.append((t, b))
-    return out
+def count_candidates_csr(name, cfg5_cands=1_000_000):
+    """The counting configs' candidate batch (this package's seeded
+    generator; == oracle.mt_episodes, tests/test_gpu_scale.py)."""
+    from paper_0905_2203_b200 import CSR, random_episodes_csr
+    if name == "cfg1":
+        return to_csr(cfg1_candidates())
+    if name not in CAND_SEQ:
+        raise SystemExit(f"{name} is not a counting config")
+    seed, nodes, alphabet = CAND_SEQ[name]
+    count = {"cfg3": 10_000, "cfg4": 10_000, "cfg5": cfg5_cands}[name]
+    csr = random_episodes_csr(seed, count, nodes, alphabet, BINS)
+    if name == "cfg4":
+        x = to_csr(CFG4_CHAINS)
+        csr = CSR(np.concatenate([csr.offsets, csr.offsets[-1] + x.offsets[1:]]),
+                  np.concatenate([csr.types, x.types]), np.concatenate([csr.low, x.low]),
+                  np.concatenate([csr.high, x.high]))
+    return csr
 
 
 def to_csr(eps):
@@ -253,44 +254,57 @@ def cpu_info():
 
 # ------------------------------------------------------------ CPU legs ----
 
-def level3_sample(types, times, size, seed=11):
-    """Seeded sample of the cfg2 level-3 candidates (the level that carries
-    98% of the work), generated with the product's host join."""
-    from paper_0905_2203_b200 import Episode, generate_candidates
+def ref_stream(name, cfg5_events):
+    """The config's stream from the REFERENCE's generate() (oracle/_ref);
+    None for cfg4 (the reference has no burst model)."""
     import oracle
-    l1 = [Episode([t], []) for t in range(26)]
-    l2 = generate_candidates(2, l1, BINS, 26)
-    csr2 = to_csr([(e.types, e.constraints) for e in l2])
-    c2 = oracle.count_batch(types, times, csr2.offsets, csr2.types, csr2.low, csr2.high,
-                            threads=os.cpu_count() or 1)
-    f2 = [e for e, c in zip(l2, c2) if c >= 250]
-    l3 = generate_candidates(3, f2, BINS, 26)
-    rng = np.random.default_rng(seed)
-    pick = np.sort(rng.choice(len(l3), size=min(size, len(l3)), replace=False))
-    return to_csr([(l3[i].types, l3[i].constraints) for i in pick]), len(l3)
+    sp = stream_spec(name, cfg5_events)
+    if sp["kind"] != "generate":
+        return None
+    t, tm = oracle.ref_generate(sp["neurons"], sp["duration_s"], sp["rate_hz"], sp["seed"], sp["embedded"])
+    return t, tm, alphabet_of(sp)
 
 
-def cpu_reference_rate(types, times, alphabet, csr, budget_s, min_reps=1):
+def ref_candidates(name, start, count):
+    """Candidates [start, start+count) of a config's seeded sequence, drawn
+    in pure Python (oracle.mt_episodes; no package code)."""
+    import oracle
+    if name == "cfg1":
+        return cfg1_candidates()[start:start + count]
+    seed, nodes, alphabet = CAND_SEQ[name]
+    return oracle.mt_episodes(seed, start + count, nodes, alphabet, BINS)[start:]
+
+
+def csr_arrays_of(eps):
+    import oracle
+    return oracle.csr_arrays(eps)
+
+
+def sample_size(name, n_events, steps):
+    """Candidates per CPU step: about 1,000 over the whole run (>= 1,000
+    distinct seeded candidates when the run has enough steps), each step a
+    few seconds of host work at most."""
+    if name == "cfg1":
+        return 676
+    per_step = max(16, -(-1000 // max(steps, 1)))
+    cap = max(16, int(4e10 // max(n_events, 1)))  # ~1e10-4e10 ee per step
+    return min(per_step, cap, 1000)
+
+
+def cpu_reference_count(types, times, alphabet, eps, cores):
     """The reference's counting path (oracle/_ref = reference headers compiled
     in place): episode-parallel count_tracking over candidates on all host
     cores, i.e. mine() with strategy_switch_level > max_level (its fastest
     configuration, SURVEY §8d "R2"). Falls back to the C port (count_fsm
     restatement, same threading) if the reference build is absent."""
     import oracle
-    cores, _ = cpu_info()
-    kind = "reference" if oracle.ref_available() else "port"
-    reps, t_total, ee = 0, 0.0, 0
-    while reps < min_reps or t_total < budget_s:
-        t0 = time.perf_counter()
-        if kind == "reference":
-            oracle.ref_count_batch(types, times, alphabet, csr.offsets, csr.types, csr.low, csr.high,
-                                   algo="tracking", workers=cores, parallel=True)
-        else:
-            oracle.count_batch(types, times, csr.offsets, csr.types, csr.low, csr.high, threads=cores)
-        t_total += time.perf_counter() - t0
-        ee += len(csr) * len(types)
-        reps += 1
-    return ee / t_total, kind, cores, reps, t_total
+    off, et, lo, hi = csr_arrays_of(eps)
+    if oracle.ref_available():
+        oracle.ref_count_batch(types, times, alphabet, off, et, lo, hi, algo="tracking", workers=cores,
+                               parallel=True)
+        return "reference"
+    oracle.count_batch(types, times, off, et, lo, hi, threads=cores)
+    return "port"
 
 
 # ------------------------------------------------------------- our arm ----
@@ -352,8 +366,7 @@ def run_ours(args, rank, world, local_rank):
         workload = {"workload": "cfg2: Sym26 mining to level 4, 3 bins, threshold 250, two-pass",
                     "events": n, "levels": 4, "threshold": 250, "bins": BINS}
     else:
-        eps = count_candidates(args.config, args.cfg5_cands)
-        csr_all = to_csr(eps)
+        csr_all = count_candidates_csr(args.config, args.cfg5_cands)
 
         if world > 1:
             # epi_count_sharded: >= 4096 episodes per rank shard by episode,
@@ -367,9 +380,8 @@ def run_ours(args, rank, world, local_rank):
                 return merged()
             ctx.count_csr(csr_all, 1, 0, shard=(rank, world, 4096 * world, ag))
             return len(csr_all) / world, ctx.last_stats  # job units, summed over ranks below
-        workload = {"workload": f"{args.config}: exact counts of {len(eps)} "
-                                f"{len(eps[0][0])}-node candidates",
-                    "events": n, "candidates": len(eps), "alphabet": alphabet}
+        workload = {"workload": workload_name(args), "events": n, "candidates": len(csr_all),
+                    "alphabet": alphabet}
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
@@ -466,14 +478,17 @@ def run_ours(args, rank, world, local_rank):
     kernels = []
     if map_ms > 0:
         ach = matched / (map_ms * 1e-3) / 1e12
-        tr, src = traffic_for("machines_kernel")
-        kernels.append({"kernel": "machines_kernel", "bound": "int32",
+        chain = sum(s.get("chain_launches", 0) for s in stats)
+        kname = "chain_kernel" if chain == map_launches else ("machines_kernel" if chain == 0 else
+                                                               "chain_kernel+machines_kernel")
+        tr, src = traffic_for(kname)
+        kernels.append({"kernel": kname, "bound": "int32",
                         "model": "matched pairs (SURVEY 8d): 1 int op per (episode, event of an episode type)",
                         "achieved": round(ach, 4), "peak": round(peak_int, 3), "unit": "Tops/s",
                         "frac": round(ach / peak_int, 5) if peak_int else None,
                         "traffic": tr, "traffic_unit": "DRAM bytes per launch (ncu)", "traffic_source": src,
                         "peak_source": "epi_probe_int32 mode 1 (LOP3+IMAD, measured in this run)",
-                        "pipe_util_ncu": pipes_for("machines_kernel"),
+                        "pipe_util_ncu": pipes_for(kname),
                         "launches": map_launches, "avg_launch_ms": round(map_ms / max(map_launches, 1), 5),
                         "device_ms": round(map_ms, 4),
                         "share_of_device_time": round(map_ms / total_dev_ms, 4) if total_dev_ms else None,
@@ -526,64 +541,108 @@ def ctypes_probe(native, device, mode=1):
     return v.value if st == 0 else 0.0
 
 
+def cpu_mine_step(types, times, cores):
+    """The reference's full mine() on cfg2 (E/miner.hpp:114-173): tracking
+    backend, episode-parallel at every level (strategy_switch_level >
+    max_level, SURVEY §8d "R2"), all host cores. Returns (candidates, csv)."""
+    import oracle
+    csv, cands, _ = oracle.ref_mine(types, times, 26, 250, BINS, 4, switch_level=99, backend=1,
+                                    workers=cores)
+    return sum(cands), csv
+
+
+def cpu_leg(args, types, times, alphabet, steps):
+    """Times the reference CPU path over `steps` bounded samples of the
+    workload; returns (value, seconds, sample description, kind)."""
+    cores, _ = cpu_info()
+    n = len(types)
+    if args.config == "cfg2":
+        units, secs = 0, 0.0
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            c, _ = cpu_mine_step(types, times, cores)
+            secs += time.perf_counter() - t0
+            units += c
+        return units * n / secs, secs, ("the reference's full mine() (levels 1-4, tracking, "
+                                        "strategy_switch_level > max_level) per step"), "reference"
+    k = sample_size(args.config, n, steps)
+    units, secs, kind = 0, 0.0, None
+    for s in range(steps):
+        eps = ref_candidates(args.config, (s * k) % 100_000 if args.config != "cfg1" else 0, k)
+        t0 = time.perf_counter()
+        kind = cpu_reference_count(types, times, alphabet, eps, cores)
+        secs += time.perf_counter() - t0
+        units += len(eps)
+    covered = min(steps * k, 100_000) if args.config != "cfg1" else 676
+    sample = (f"{k} candidates per step of the config's seeded sequence (step s: candidates "
+              f"[s*{k}, (s+1)*{k}), {covered} distinct over the run) x all {n} events; count_tracking "
+              "episode-parallel (mine() with strategy_switch_level > max_level); rate extrapolated "
+              "linearly to the whole candidate set")
+    return units * n / secs, secs, sample, kind
+
+
 def cpu_baseline_for(args, types, times, alphabet):
     cores, model = cpu_info()
-    if args.config == "cfg2":
-        csr, n3 = level3_sample(types, times, 20000)
-        sample = (f"{len(csr)} seeded cfg2 level-3 candidates (of {n3}) x {len(types)} events, "
-                  "count_tracking episode-parallel on all cores")
-    elif args.config == "cfg1":
-        csr = to_csr(cfg1_candidates())
-        sample = f"all 676 cfg1 candidates x {len(types)} events"
-    elif args.config == "cfg3":
-        csr = to_csr(cfg3_candidates(64))
-        sample = f"first 64 cfg3 candidates x {len(types)} events"
-    else:
-        k = 16 if len(types) > 50_000_000 else 64
-        csr = to_csr(count_candidates(args.config, args.cfg5_cands)[:k])
-        sample = f"first {k} {args.config} candidates x {len(types)} events"
-    rate, kind, cores, reps, secs = cpu_reference_rate(types, times, alphabet, csr, args.cpu_seconds)
-    return {"value": rate, "unit": "episode-events/s", "cores": cores, "kind": kind,
-            "sample": f"{sample}; {reps} reps in {secs:.1f} s", "cpu": model}
+    steps = 1 if args.config == "cfg2" else max(1, -(-1000 // sample_size(args.config, len(types), 1)))
+    value, secs, sample, kind = cpu_leg(args, types, times, alphabet, steps)
+    return {"value": value, "unit": "episode-events/s", "cores": cores, "kind": kind,
+            "sample": f"{sample}; {steps} step(s) in {secs:.1f} s", "cpu": model}
 
 
 def run_reference(args):
-    types, times, alphabet = make_stream(args.config, args.cfg5_events)
+    """--impl reference: the reference's own CPU implementation only
+    (oracle/_ref: generate(), count_tracking / mine()); this package is not
+    imported."""
+    import oracle
     cores, model = cpu_info()
+    base = {"metric": "episode-events counted/sec (device-timed)", "impl": "reference", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic", "unit": "episode-events/s"}
+    if not oracle.ref_available():
+        return dict(base, unavailable="oracle/_ref/libepisodic_ref.so not built (needs /root/reference)")
+    st = ref_stream(args.config, args.cfg5_events)
+    if st is None:
+        return dict(base, unavailable="cfg4's bursty MEA-shaped stream has no reference generator")
+    types, times, alphabet = st
+    n = len(types)
     if args.config == "cfg2":
-        csr, n3 = level3_sample(types, times, 20000)
-        sample = f"{len(csr)} seeded cfg2 level-3 candidates (of {n3})"
-    elif args.config == "cfg1":
-        csr = to_csr(cfg1_candidates())
-        sample = "all 676 cfg1 candidates"
-    elif args.config == "cfg3":
-        csr = to_csr(cfg3_candidates(64))
-        sample = "first 64 cfg3 candidates"
+        cpu_leg(args, types, times, alphabet, 1)  # warm-up: one mine()
+        value, secs, sample, kind = cpu_leg(args, types, times, alphabet, args.steps)
+        cands = None
     else:
-        k = 16 if len(types) > 50_000_000 else 64
-        csr = to_csr(count_candidates(args.config, args.cfg5_cands)[:k])
-        sample = f"first {k} {args.config} candidates"
-    for _ in range(args.warmup):
-        cpu_reference_rate(types, times, alphabet, csr, 0.0)
-    rates = []
-    kind = None
-    t_all = 0.0
-    for _ in range(args.steps):
-        r, kind, cores, reps, secs = cpu_reference_rate(types, times, alphabet, csr, 0.0)
-        rates.append(r)
-        t_all += secs
-    value = len(csr) * len(types) * args.steps / t_all
-    return {"metric": "episode-events counted/sec (device-timed)", "impl": "reference",
-            "value": value, "unit": "episode-events/s", "n_gpus": 1, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_all / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (reference CPU: {sample})", "events": len(types)},
-            "cpu_baseline": {"value": value, "unit": "episode-events/s", "cores": cores, "kind": kind,
-                             "sample": f"{sample} x {len(types)} events per step, count_tracking "
-                                       "episode-parallel (mine() with strategy_switch_level > "
-                                       "max_level) on all cores", "cpu": model},
-            "e2e": {"value": value, "unit": "episode-events/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+        k = sample_size(args.config, n, args.steps)
+        cpu_reference_count(types, times, alphabet, ref_candidates(args.config, 0, min(k, 16)), cores)
+        value, secs, sample, kind = cpu_leg(args, types, times, alphabet, args.steps)
+        cands = {"cfg1": 676, "cfg3": 10_000, "cfg4": 10_002, "cfg5": args.cfg5_cands}[args.config]
+    ms = secs / args.steps * 1e3
+    cfg = {"workload": workload_name(args), "events": n, "reference_sample": sample}
+    if cands:
+        cfg["candidates"] = cands
+    return dict(base, value=value, ms_per_step=ms, config=cfg,
+                cpu_baseline={"value": value, "unit": "episode-events/s", "cores": cores, "kind": kind,
+                              "sample": sample, "cpu": model},
+                e2e={"value": value, "unit": "episode-events/s", "h2d_bytes_per_step": 0,
+                     "d2h_bytes_per_step": 0},
+                native_so_loaded=loaded_native_libs())
+
+
+def loaded_native_libs():
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so") and ROOT in ln})
+    except OSError:
+        return []
+
+
+def workload_name(args):
+    if args.config == "cfg2":
+        return "cfg2: Sym26 mining to level 4, 3 bins, threshold 250, two-pass"
+    if args.config == "cfg5":
+        return (f"cfg5 cell: {args.cfg5_events} events x {args.cfg5_cands} seeded 3-node candidates, "
+                "exact counts")
+    return {"cfg1": "cfg1: Sym26, all 676 2-node candidates, exact counts",
+            "cfg3": "cfg3: 10M events x 10,000 seeded 3-node candidates, exact counts",
+            "cfg4": "cfg4: MEA-shaped ~100M bursty events x 10,002 5-node candidates, exact counts"}[args.config]
 
 
 def main():
@@ -592,9 +651,9 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--config", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--cfg5-events", type=int, default=10_000_000, help="cfg5 cell: stream length")
-    ap.add_argument("--cfg5-cands", type=int, default=10_000, help="cfg5 cell: 3-node candidates")
+    ap.add_argument("--cfg5-cands", type=int, default=1_000_000, help="cfg5 cell: 3-node candidates")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -79,6 +79,7 @@ typedef struct {
   uint64_t bound_words;       /* pass-1 popcount bound: (candidate, 32 ms tile)
                                  AND-POPC word pairs                            */
   double bound_ms;            /* device time of the pass-1 bound kernels       */
+  uint64_t chain_launches;    /* map launches that ran the chain kernel         */
 } epi_stats;
 
 /* Context bound to one CUDA device. */

@@ -39,7 +39,8 @@ class Stats(C.Structure):
                 ("tile_steps", C.c_uint64), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("pass1_ms", C.c_double), ("pass2_ms", C.c_double), ("map_ms", C.c_double),
                 ("concat_ms", C.c_double), ("total_ms", C.c_double),
-                ("bound_words", C.c_uint64), ("bound_ms", C.c_double)]
+                ("bound_words", C.c_uint64), ("bound_ms", C.c_double),
+                ("chain_launches", C.c_uint64)]
 
     _names = None
 

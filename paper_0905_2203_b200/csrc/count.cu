@@ -7,6 +7,37 @@
 #include "count_impl.cuh"
 
 namespace epi {
+namespace impl {
+template <int W>
+bool launch_chain_w(int n, const CountLaunch& p, cudaStream_t st);
+}
+
+#define EPI_EXTERN_C(W) \
+  extern template bool impl::launch_chain_w<W>(int, const CountLaunch&, cudaStream_t);
+EPI_EXTERN_C(1) EPI_EXTERN_C(2) EPI_EXTERN_C(3) EPI_EXTERN_C(4)
+EPI_EXTERN_C(5) EPI_EXTERN_C(6) EPI_EXTERN_C(7) EPI_EXTERN_C(8)
+EPI_EXTERN_C(9) EPI_EXTERN_C(10) EPI_EXTERN_C(11) EPI_EXTERN_C(12)
+EPI_EXTERN_C(13) EPI_EXTERN_C(14) EPI_EXTERN_C(15) EPI_EXTERN_C(16)
+#undef EPI_EXTERN_C
+
+bool has_chain_kernel(int n_nodes, int width, bool hi32) {
+  return hi32 && n_nodes >= 2 && n_nodes <= 8 && width >= 1 && width <= 16;
+}
+
+bool launch_chain(int n_nodes, int width, const CountLaunch& p, cudaStream_t st) {
+  if (!has_chain_kernel(n_nodes, width, true)) return false;
+  switch (width) {
+#define EPI_CASE_C(W) \
+  case W:             \
+    return impl::launch_chain_w<W>(n_nodes, p, st);
+    EPI_CASE_C(1) EPI_CASE_C(2) EPI_CASE_C(3) EPI_CASE_C(4)
+    EPI_CASE_C(5) EPI_CASE_C(6) EPI_CASE_C(7) EPI_CASE_C(8)
+    EPI_CASE_C(9) EPI_CASE_C(10) EPI_CASE_C(11) EPI_CASE_C(12)
+    EPI_CASE_C(13) EPI_CASE_C(14) EPI_CASE_C(15) EPI_CASE_C(16)
+#undef EPI_CASE_C
+  }
+  return false;
+}
 
 #define EPI_EXTERN_W(W) \
   extern template void impl::launch_machines_w<W>(int, const CountLaunch&, cudaStream_t);

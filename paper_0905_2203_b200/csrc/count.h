@@ -41,6 +41,8 @@ struct CountLaunch {
   int32_t map_segs;          // 0: all P segments
   const unsigned long long* hist;  // events per type (matched-pair statistics), may be null
   unsigned long long* matched;     // += sum over live episodes of sum_k hist[type_k]
+  const uint32_t* out_perm;  // non-null: episode e's count goes to counts[out_perm[e]]
+  int32_t chain_depth;       // chain kernel test knob: d + 1 forces prefix depth d (0: auto)
 };
 
 // Doubling-smear shift amounts covering a window of width w (1..16).
@@ -67,6 +69,11 @@ bool launch_machines_last(int n_nodes, int width, uint32_t w_last, CountLaunch& 
 // high > 63 (up to kMaxHighWide): local-memory history ring.
 void launch_machines_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
 void launch_walk_wide(int n_nodes, const CountLaunch& p, cudaStream_t st);
+// Chain map kernel (chain_impl.cuh): every window of width `width` (1..16),
+// every high <= 32, 2..8 nodes, host-sized launch. Returns false (nothing
+// launched) for other shapes.
+bool launch_chain(int n_nodes, int width, const CountLaunch& p, cudaStream_t st);
+bool has_chain_kernel(int n_nodes, int width, bool hi32);
 // Exact counts of single-node episodes (popcount of the type's bitmap).
 void launch_singletons(const uint32_t* occ, uint32_t blk_words, uint32_t n_blocks,
                        const uint32_t* types, uint32_t n_eps, uint64_t* counts, cudaStream_t st);

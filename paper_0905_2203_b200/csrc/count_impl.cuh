@@ -87,6 +87,10 @@ __device__ __forceinline__ uint32_t live_eps(const CountLaunch& p) {
   return p.n_dev ? *p.n_dev : p.n_eps;
 }
 
+__device__ __forceinline__ uint32_t out_index(const CountLaunch& p, uint32_t e) {
+  return p.out_perm ? p.out_perm[e] : e;
+}
+
 __device__ __forceinline__ size_t occ_index(int32_t g, uint32_t type, uint32_t blk_words) {
   return static_cast<size_t>(g >> 5) * blk_words + type * kRowStride + (g & 31);
 }
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
 
   if (active) {
     if (p.P == 1) {
-      p.counts[e] = cnt;  // one segment from the stream start: exact, no walk
+      p.counts[out_index(p, e)] = cnt;  // one segment from the stream start: exact, no walk
     } else {
       const size_t idx = static_cast<size_t>(q) * p.n_eps + e;
       p.f_count[idx] = cnt;
@@ -695,7 +699,7 @@ __global__ void __launch_bounds__(128) walk_kernel(const CountLaunch p) {
     restart = restarts_next(p, q, cnt, last, ep.sigma);
     L = last;
   }
-  p.counts[e] = total;
+  p.counts[out_index(p, e)] = total;
   // statistics: one atomic per warp (per-thread atomics on one address
   // serialise in L2)
   const unsigned mask = __activemask();
@@ -771,7 +775,7 @@ __device__ __forceinline__ void walk_warp_episode(const CountLaunch& p, uint32_t
   for (int i = 0; i < kWalkWarpSegs; ++i) total += cnt[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-  if (lane == 0) p.counts[e] = total;
+  if (lane == 0) p.counts[out_index(p, e)] = total;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) patches += __shfl_xor_sync(0xffffffffu, patches, o);
   if (lane == 0 && patches) atomicAdd(p.patches, static_cast<unsigned long long>(patches));

@@ -12,11 +12,14 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <thread>
 #include <unordered_map>
 
+#include "chain_sort.h"
 #include "count.h"
 
 namespace epi {
@@ -30,16 +33,12 @@ enum Slot : size_t {
   kSlotSegments = 6,
   kSlotShardStage = 7,
   kSlotShardCounts = 8,
+  kSlotChainSort = 9,
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-void validate_constraint(int64_t lo, int64_t hi) {
-  if (lo < 0 || lo >= hi)
-    throw Error(EPI_EINVAL, "interval constraint requires 0 <= low < high");
-}
 
 uint64_t hash_span(const uint32_t* t, size_t nt, const int64_t* lo, const int64_t* hi, size_t nc) {
   uint64_t h = 0x9e3779b97f4a7c15ull ^ (nt * 0x100000001b3ull);
@@ -249,6 +248,94 @@ void Engine::load_stream_device(const uint32_t* d_types, const int64_t* d_times,
   stream_.load(n, alphabet, st_, scratch_);
 }
 
+// Packs n episodes of N nodes into the counting kernels' parameter layout
+// (types clamped to the spare zero row `alphabet`, windows (low+1) | high<<16,
+// sums of highs) in parallel over host threads, and summarises the launch
+// shape (max high, max sigma, uniform widths) in `ds`. Types outside the
+// alphabet can never fire; they read the always-zero spare column.
+template <class TypeAt, class LoAt, class HiAt>
+void pack_episodes(size_t n, uint32_t N, uint32_t A, uint32_t* h_types, uint32_t* h_win, uint32_t* h_sigma,
+                   DevSet& ds, TypeAt&& type_at, LoAt&& lo_at, HiAt&& hi_at) {
+  const uint32_t M = N - 1;
+  struct Part {
+    int64_t max_high = 0;
+    uint32_t max_sigma = 0;
+    int64_t width = -1, width_last = -1;  // -1 unset, 0 mixed
+    bool too_wide = false;
+  };
+  unsigned w = std::thread::hardware_concurrency();
+  w = std::min<unsigned>(w ? w : 1, 32);
+  std::vector<Part> parts(w);
+  std::atomic<unsigned> next{0};
+  host_parallel(n, n >= 65536, [&](size_t b, size_t e) {
+    Part& pt = parts[next.fetch_add(1)];
+    for (size_t i = b; i < e; ++i) {
+      for (uint32_t k = 0; k < N; ++k) {
+        const uint32_t t = type_at(i, k);
+        h_types[i * N + k] = t < A ? t : A;
+      }
+      uint32_t sig = 0;
+      for (uint32_t k = 0; k < M; ++k) {
+        const int64_t lo = lo_at(i, k), hi = hi_at(i, k);
+        if (hi > kMaxHighWide) pt.too_wide = true;
+        h_win[i * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
+        sig += static_cast<uint32_t>(hi);
+        pt.max_high = std::max(pt.max_high, hi);
+        int64_t& wd = k + 1 < M ? pt.width : pt.width_last;
+        if (wd == -1)
+          wd = hi - lo;
+        else if (wd != hi - lo)
+          wd = 0;
+      }
+      h_sigma[i] = sig;
+      pt.max_sigma = std::max(pt.max_sigma, sig);
+    }
+  });
+  int64_t width = -1, width_last = -1;
+  auto merge = [](int64_t& a, int64_t b) {
+    if (b == -1) return;
+    if (a == -1)
+      a = b;
+    else if (a != b)
+      a = 0;
+  };
+  for (unsigned i = 0; i < next.load(); ++i) {
+    const Part& pt = parts[i];
+    if (pt.too_wide)
+      throw Error(EPI_EUNSUPPORTED, "constraint high > 4095 ms is not supported by the device counter");
+    ds.max_high = std::max(ds.max_high, pt.max_high);
+    ds.max_sigma = std::max(ds.max_sigma, pt.max_sigma);
+    merge(width, pt.width);
+    merge(width_last, pt.width_last);
+  }
+  if (width == -1 || width == width_last) {
+    ds.width = width_last > 0 ? static_cast<int>(width_last) : 0;
+  } else if (width > 0 && width_last > 0) {
+    ds.width = static_cast<int>(width);  // the last constraint alone differs
+    ds.last_w = static_cast<uint32_t>(width_last);
+  }
+}
+
+void Engine::count_packed(DevSet ds, char* host, size_t off_win, size_t off_sigma, size_t total, uint64_t* out,
+                          epi_stats& stats, double* ms_out) {
+  const size_t n = ds.n;
+  char* d_params = scratch_.get<char>(kSlotParams, total);
+  EPI_CUDA(cudaMemcpyAsync(d_params, host, total, cudaMemcpyHostToDevice, st_));
+  stats.h2d_bytes += total;
+  ds.types = reinterpret_cast<const uint32_t*>(d_params);
+  ds.win = reinterpret_cast<const uint32_t*>(d_params + off_win);
+  ds.sigma = reinterpret_cast<const uint32_t*>(d_params + off_sigma);
+  uint64_t* d_counts = scratch_.get<uint64_t>(kSlotCounts, n);
+  count_device(ds, d_counts, stats, ms_out);
+  uint64_t* h_counts = static_cast<uint64_t*>(pin_down_.get(n * sizeof(uint64_t)));
+  EPI_CUDA(cudaMemcpyAsync(h_counts, d_counts, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaStreamSynchronize(st_));
+  host_parallel(n, n >= (1u << 18), [&](size_t b, size_t e) {
+    std::memcpy(out + b, h_counts + b, (e - b) * sizeof(uint64_t));
+  });
+  stats.d2h_bytes += n * sizeof(uint64_t);
+}
+
 void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                          double* ms_out) {
   const size_t n = set.size();
@@ -258,66 +345,42 @@ void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, e
     throw Error(EPI_EUNSUPPORTED, "episodes longer than 16 nodes are not supported on the device path");
   const uint32_t N = set.N;
   const uint32_t M = N - 1;
-
-  // Pack episode parameters. Types outside the alphabet can never fire; they
-  // read the always-zero spare column `alphabet` of every tile row.
-  const size_t off_types = 0;
-  const size_t off_win = align_up(off_types + n * N * 4, 256);
+  const size_t off_win = align_up(n * N * 4, 256);
   const size_t off_sigma = align_up(off_win + n * M * 4, 256);
   const size_t total = align_up(off_sigma + n * 4, 256);
   char* host = static_cast<char*>(pin_up_.get(total));
-  uint32_t* h_types = reinterpret_cast<uint32_t*>(host + off_types);
-  uint32_t* h_win = reinterpret_cast<uint32_t*>(host + off_win);
-  uint32_t* h_sigma = reinterpret_cast<uint32_t*>(host + off_sigma);
   DevSet ds;
   ds.N = N;
   ds.n = n;
-  const uint32_t A = stream_.alphabet;
-  // launch-uniform window width high-low of the constraints before the last
-  // (width) and of the last one (width_last); -1 unset, 0 mixed
-  int64_t width = -1, width_last = -1;
-  for (size_t e = 0; e < n; ++e) {
-    for (uint32_t k = 0; k < N; ++k) {
-      uint32_t t = set.types[e * N + k];
-      h_types[e * N + k] = t < A ? t : A;
-    }
-    uint32_t sig = 0;
-    for (uint32_t k = 0; k < M; ++k) {
-      int64_t lo = set.lo[e * M + k], hi = set.hi[e * M + k];
-      if (hi > kMaxHighWide)
-        throw Error(EPI_EUNSUPPORTED, "constraint high > 4095 ms is not supported by the device counter");
-      h_win[e * M + k] = static_cast<uint32_t>(lo + 1) | (static_cast<uint32_t>(hi) << 16);
-      sig += static_cast<uint32_t>(hi);
-      ds.max_high = std::max(ds.max_high, hi);
-      int64_t& w = k + 1 < M ? width : width_last;
-      if (w == -1)
-        w = hi - lo;
-      else if (w != hi - lo)
-        w = 0;
-    }
-    h_sigma[e] = sig;
-    ds.max_sigma = std::max(ds.max_sigma, sig);
-  }
-  if (width == -1 || width == width_last) {
-    ds.width = width_last > 0 ? static_cast<int>(width_last) : 0;
-  } else if (width > 0 && width_last > 0) {
-    ds.width = static_cast<int>(width);  // the last constraint alone differs
-    ds.last_w = static_cast<uint32_t>(width_last);
-  }
-  char* d_params = scratch_.get<char>(kSlotParams, total);
-  EPI_CUDA(cudaMemcpyAsync(d_params, host, total, cudaMemcpyHostToDevice, st_));
-  stats.h2d_bytes += total;
-  ds.types = reinterpret_cast<const uint32_t*>(d_params + off_types);
-  ds.win = reinterpret_cast<const uint32_t*>(d_params + off_win);
-  ds.sigma = reinterpret_cast<const uint32_t*>(d_params + off_sigma);
+  pack_episodes(
+      n, N, stream_.alphabet, reinterpret_cast<uint32_t*>(host), reinterpret_cast<uint32_t*>(host + off_win),
+      reinterpret_cast<uint32_t*>(host + off_sigma), ds, [&](size_t e, uint32_t k) { return set.types[e * N + k]; },
+      [&](size_t e, uint32_t k) { return set.lo[e * M + k]; }, [&](size_t e, uint32_t k) { return set.hi[e * M + k]; });
+  count_packed(ds, host, off_win, off_sigma, total, counts.data(), stats, ms_out);
+}
 
-  uint64_t* d_counts = scratch_.get<uint64_t>(kSlotCounts, n);
-  count_device(ds, d_counts, stats, ms_out);
-  uint64_t* h_counts = static_cast<uint64_t*>(pin_down_.get(n * sizeof(uint64_t)));
-  EPI_CUDA(cudaMemcpyAsync(h_counts, d_counts, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, st_));
-  EPI_CUDA(cudaStreamSynchronize(st_));
-  std::memcpy(counts.data(), h_counts, n * sizeof(uint64_t));
-  stats.d2h_bytes += n * sizeof(uint64_t);
+void Engine::count_exact_csr(const epi_episode_batch& b, uint32_t N, uint64_t* counts_out, epi_stats& stats,
+                             double* ms_out) {
+  const size_t n = b.n_episodes;
+  if (n == 0) return;
+  if (N > static_cast<uint32_t>(kMaxNodes))
+    throw Error(EPI_EUNSUPPORTED, "episodes longer than 16 nodes are not supported on the device path");
+  const uint32_t M = N - 1;
+  const size_t off_win = align_up(n * N * 4, 256);
+  const size_t off_sigma = align_up(off_win + n * M * 4, 256);
+  const size_t total = align_up(off_sigma + n * 4, 256);
+  char* host = static_cast<char*>(pin_up_.get(total));
+  DevSet ds;
+  ds.N = N;
+  ds.n = n;
+  // episode e: nodes at offsets[e] + k, constraints at offsets[e] - e + k
+  const uint32_t* off = b.offsets;
+  pack_episodes(
+      n, N, stream_.alphabet, reinterpret_cast<uint32_t*>(host), reinterpret_cast<uint32_t*>(host + off_win),
+      reinterpret_cast<uint32_t*>(host + off_sigma), ds, [&](size_t e, uint32_t k) { return b.types[off[e] + k]; },
+      [&](size_t e, uint32_t k) { return b.low[off[e] - e + k]; },
+      [&](size_t e, uint32_t k) { return b.high[off[e] - e + k]; });
+  count_packed(ds, host, off_win, off_sigma, total, counts_out, stats, ms_out);
 }
 
 // Exact counts of a device-resident set into d_counts (device). Plans the
@@ -363,7 +426,31 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   p.ep_win = ds.win;
   p.ep_sigma = ds.sigma;
   p.counts = d_counts;
+  // Chain map kernel (chain_impl.cuh): host-sized launches with one window
+  // width (<= 16) and every high <= 32. The episodes are counted in a sorted
+  // order (shared chain prefixes per CTA); counts scatter back through perm.
+  // EPI_CHAIN=0 keeps the automaton kernel, EPI_CHAIN=1 uses the chain kernel
+  // on sets of any size (tests), EPI_CHAIN_DEPTH=d+1 forces prefix depth d.
+  const char* chain_env = std::getenv("EPI_CHAIN");
+  const uint64_t chain_min = chain_env ? (std::atoi(chain_env) == 1 ? 1 : ~0ull) : 1024;
+  const bool chain = !wide && !ds.last_w && live_slot < 0 && n >= chain_min && p.stages > 0 &&
+                     has_chain_kernel(static_cast<int>(N), ds.width, ds.max_high <= 32);
+  if (chain) {
+    char* sc = scratch_.get<char>(kSlotChainSort, chain_sort_scratch(n, N));
+    ChainSortOut so{};
+    const int own = chain_sort({ds.types, ds.win, ds.sigma, n, N, stream_.alphabet}, sc, so, st_);
+    stats.kernel_launches += static_cast<uint64_t>(own);
+    p.ep_types = so.types;
+    p.ep_win = so.win;
+    p.ep_sigma = so.sigma;
+    p.out_perm = so.perm;
+    if (const char* dd = std::getenv("EPI_CHAIN_DEPTH")) p.chain_depth = std::atoi(dd);
+  }
   auto launch_map = [&]() {
+    if (chain) {
+      launch_chain(static_cast<int>(N), ds.width, p, st_);
+      return;
+    }
     if (wide)
       launch_machines_wide(static_cast<int>(N), p, st_);
     else if (ds.last_w && ds.max_high <= 32 &&
@@ -393,7 +480,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
                          (static_cast<uint64_t>(ds.max_high <= 32) << 39) ^
                          (static_cast<uint64_t>(wide) << 38) ^
                          (static_cast<uint64_t>(p.stages) << 32) ^ p.blk_words ^
-                         (static_cast<uint64_t>(ds.last_w) << 56);
+                         (static_cast<uint64_t>(ds.last_w) << 56) ^ (static_cast<uint64_t>(chain) << 37);
   int bps = 0;
   for (const auto& kv : occ_cache_)
     if (kv.first == shape) bps = kv.second;
@@ -455,6 +542,9 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     P = std::min<int64_t>(max_p, (std::max<int64_t>(P, ts->world) + ts->world - 1) / ts->world * ts->world);
   else
     ts = nullptr;  // stream too short to give every rank a segment: every rank maps all
+  // The chain kernel keeps times relative to a segment's window start in
+  // 32 bits: segments (plus window) shorter than 2^26 tiles.
+  if (chain) P = std::max<int64_t>(P, (tiles4 + (int64_t{1} << 25) - 1) >> 25);
   // Segment bounds are multiples of 4 tiles (the map kernel advances four
   // tiles per 16-byte load); the last segment runs to the 4-aligned end (the
   // bitmap is zero past the stream).
@@ -531,6 +621,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   stats.segments = static_cast<uint64_t>(P);
   stats.kernel_launches += P > 1 ? 2 : 1;  // map (+ walk)
   stats.map_launches += 1;
+  if (chain) stats.chain_launches += 1;
 }
 
 void Engine::count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
@@ -637,15 +728,53 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
   require_stream();
   begin_op();
   if (mode > EPI_MODE_MINE) throw Error(EPI_EINVAL, "epi_count: unknown mode");
-  // validate(Episode) for every candidate first (E/types.hpp:87-92).
+  // validate(Episode) for every candidate first (E/types.hpp:87-92), in
+  // parallel; the first offender in candidate order decides the error
   std::vector<uint32_t> lens(n);
-  for (uint64_t e = 0; e < n; ++e) {
-    if (b.offsets[e + 1] < b.offsets[e]) throw Error(EPI_EINVAL, "epi_count: offsets not monotone");
-    uint32_t N = b.offsets[e + 1] - b.offsets[e];
-    if (N == 0) throw Error(EPI_EINVAL, "episode must have at least one node");
-    const uint64_t cb = b.offsets[e] - e;
-    for (uint32_t k = 0; k + 1 < N; ++k) validate_constraint(b.low[cb + k], b.high[cb + k]);
-    lens[e] = N;
+  std::atomic<uint64_t> first_bad{UINT64_MAX};
+  std::vector<int> bad_kind(n ? 1 : 0);
+  std::mutex bad_mu;
+  host_parallel(n, n >= 65536, [&](size_t lo_e, size_t hi_e) {
+    for (uint64_t e = lo_e; e < hi_e; ++e) {
+      int kind = 0;
+      if (b.offsets[e + 1] < b.offsets[e]) {
+        kind = 1;
+      } else {
+        const uint32_t N = b.offsets[e + 1] - b.offsets[e];
+        lens[e] = N;
+        if (N == 0) kind = 2;
+        const uint64_t cb = b.offsets[e] - e;
+        for (uint32_t k = 0; kind == 0 && k + 1 < N; ++k)
+          if (b.low[cb + k] < 0 || b.low[cb + k] >= b.high[cb + k]) kind = 3;
+      }
+      if (kind) {
+        std::lock_guard<std::mutex> lk(bad_mu);
+        if (e < first_bad.load()) {
+          first_bad.store(e);
+          bad_kind[0] = kind;
+        }
+        return;
+      }
+    }
+  });
+  if (first_bad.load() != UINT64_MAX) {
+    static const char* kMsg[4] = {"", "epi_count: offsets not monotone", "episode must have at least one node",
+                                  "interval constraint requires 0 <= low < high"};
+    throw Error(EPI_EINVAL, kMsg[bad_kind[0]]);
+  }
+  // one episode length and exact counts (the bench's and most callers'
+  // batches): pack straight from the caller's arrays
+  bool uniform = n > 0;
+  for (uint64_t e = 0; uniform && e < n; ++e) uniform = lens[e] == lens[0];
+  if (uniform && (mode != EPI_MODE_MINE || threshold <= 1 || lens[0] <= 1)) {
+    stats.episodes += n;
+    stats.pass2_episodes += n;
+    count_exact_csr(b, lens[0], counts_out, stats, &stats.pass2_ms);
+    if (frequent_out)
+      for (uint64_t e = 0; e < n; ++e) frequent_out[e] = counts_out[e] >= threshold;
+    flush_stats(stats);
+    if (stats_out) *stats_out = stats;
+    return;
   }
   std::vector<uint32_t> distinct(lens.begin(), lens.end());
   std::sort(distinct.begin(), distinct.end());

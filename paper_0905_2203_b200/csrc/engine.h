@@ -123,6 +123,14 @@ class Engine {
 
  private:
   // Exact count of one fixed-length set on the device.
+  // Same for a batch whose episodes all have N nodes, straight from the
+  // caller's CSR (parallel host packing) into counts_out.
+  void count_exact_csr(const epi_episode_batch& b, uint32_t N, uint64_t* counts_out, epi_stats& stats,
+                       double* ms_out);
+  // Uploads packed parameters (pinned host, `total` bytes), counts them and
+  // copies the counts into out[0..n).
+  void count_packed(DevSet ds, char* host, size_t off_win, size_t off_sigma, size_t total, uint64_t* out,
+                    epi_stats& stats, double* ms_out);
   void count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                    double* ms_out);
   // Launches only: timings and counters are resolved by flush_stats.

@@ -1296,6 +1296,7 @@ void stats_axpy(epi_stats& a, const epi_stats& b, int sign) {
   const double bd[] = {b.pass1_ms, b.pass2_ms, b.map_ms, b.concat_ms, b.total_ms, b.bound_ms};
   for (int i = 0; i < 6; ++i) *ad[i] += sign * bd[i];
   a.bound_words += sign > 0 ? b.bound_words : (0 - b.bound_words);
+  a.chain_launches += sign > 0 ? b.chain_launches : (0 - b.chain_launches);
 }
 }  // namespace
 

@@ -1,35 +1,67 @@
-"""Parity at the BASELINE.json scales (configs 3-5): seeded candidate subsets
-against the oracle port on the full streams, plus size-independent
-properties of the counting semantics checked on every candidate:
+"""Parity at the BASELINE.json scales (configs 3-5) against the REFERENCE:
+tests/golden/scale.json holds counts computed by the unmodified reference
+(oracle/_ref, count_fsm on all host cores; oracle/make_scale_golden.py) on
+the full-size streams:
+  * cfg3: every one of the 10,000 candidates;
+  * cfg4 (MEA-shaped, ~100M events): the first 1,000 seeded 5-node
+    candidates + the two embedded chains;
+  * cfg5 cells (1M .. 1B events): the first 1,000 candidates of the seeded
+    sequence every cell draws from (so the subset of every |C| cell, up to
+    the 10M x 1M headline cell).
+Plus size-independent properties of the counting semantics on every
+candidate of a cell:
   * idempotent ties: duplicating every event leaves every count unchanged
     (same-type ties collapse);
   * time-shift invariance: adding a constant to every timestamp;
   * gap invariance: stretching every gap longer than the largest window;
   * prefix monotonicity: a prefix never counts more than the whole stream.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
 import oracle
 from helpers import csr_of
-from paper_0905_2203_b200 import BurstConfig, Embedding, Episode, GenConfig, generate_arrays, generate_bursty_arrays
+from paper_0905_2203_b200 import (BurstConfig, Embedding, Episode, GenConfig, generate_arrays,
+                                  generate_bursty_arrays, random_episodes_csr)
 
 pytestmark = pytest.mark.gpu
 
 BINS = [(0, 5), (5, 10), (10, 15)]
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "scale.json")
 
 
-def random_candidates(rng, n, alphabet, nodes):
-    return [([int(x) for x in rng.integers(0, alphabet, nodes)],
-             [BINS[int(b)] for b in rng.integers(0, 3, nodes - 1)]) for _ in range(n)]
+@pytest.fixture(scope="module")
+def scale():
+    with open(GOLDEN) as f:
+        return json.load(f)
 
 
-def check_subset(types, times, eps, got, k, seed):
-    rng = np.random.default_rng(seed)
-    pick = np.sort(rng.choice(len(eps), size=min(k, len(eps)), replace=False))
-    sub = csr_of([eps[i] for i in pick])
-    want = oracle.count_batch(types, times, sub.offsets, sub.types, sub.low, sub.high, threads=16)
-    np.testing.assert_array_equal(got[pick], want)
+def stream_of(cell):
+    s = cell["stream"]
+    if s["kind"] == "generate":
+        types, times = generate_arrays(GenConfig(s["neurons"], s["duration_s"], s["rate_hz"], [], s["seed"]))
+    else:
+        emb = [Embedding(Episode(t, [tuple(c) for c in cs]), s["embedded_rate_hz"]) for t, cs in cell["extra"]]
+        types, times = generate_bursty_arrays(BurstConfig(electrodes=s["electrodes"], duration_s=s["duration_s"],
+                                                          seed=s["seed"], embedded=emb))
+    assert len(types) == cell["n"]
+    assert oracle.fnv_stream(types, times, cell["alphabet"]) == cell["stream_fnv"]
+    return types, times
+
+
+def cands_of(cell, count=None):
+    c = cell["cands"]
+    csr = random_episodes_csr(c["seed"], count or c["count"], c["nodes"], c["alphabet"], BINS)
+    if cell["extra"] and count is None:
+        extra = csr_of([(t, [tuple(x) for x in cs]) for t, cs in cell["extra"]])
+        off = np.concatenate([csr.offsets, csr.offsets[-1] + extra.offsets[1:]])
+        from paper_0905_2203_b200 import CSR
+        csr = CSR(off, np.concatenate([csr.types, extra.types]), np.concatenate([csr.low, extra.low]),
+                  np.concatenate([csr.high, extra.high]))
+    return csr
 
 
 def properties(ctx, types, times, alphabet, csr, base):
@@ -50,45 +82,58 @@ def properties(ctx, types, times, alphabet, csr, base):
     assert np.all(ctx.count_csr(csr) <= base)
 
 
-def test_cfg3_full_stream_properties(ctx):
-    """cfg3: 10,004,428 events, 64 types; 2,000 seeded 3-node candidates."""
-    types, times = generate_arrays(GenConfig(64, 7813, 20, [], 3))
-    rng = np.random.default_rng(33)
-    eps = random_candidates(rng, 2000, 64, 3)
-    csr = csr_of(eps)
-    ctx.load_arrays(types, times, 64)
-    base = ctx.count_csr(csr)
-    check_subset(types, times, eps, base, 48, 1)
-    properties(ctx, types, times, 64, csr, base)
+def test_scale_candidates_match_reference_draws(scale):
+    """The product's seeded candidate generator == the fixture's draws
+    (pure-Python mt19937_64 in the reference's order)."""
+    for name in ("cfg3", "cfg4", "cfg5_1000000"):
+        c = scale[name]["cands"]
+        eps = oracle.mt_episodes(c["seed"], 50, c["nodes"], c["alphabet"], BINS)
+        got = cands_of(scale[name], 50)
+        np.testing.assert_array_equal(got.types, np.concatenate([t for t, _ in eps]))
+        np.testing.assert_array_equal(got.high, np.array([x[1] for _, cs in eps for x in cs]))
 
 
-def test_cfg4_mea_bursty_100m(ctx):
-    """cfg4: MEA-shaped, 60 electrodes, ~100M events with network bursts;
-    5-node candidates (random + the embedded chains)."""
-    chains = [Episode([0, 7, 13, 21, 33], [(5, 10), (0, 5), (10, 15), (5, 10)]),
-              Episode([40, 41, 42, 43, 44], [(0, 5)] * 4)]
-    cfg = BurstConfig(electrodes=60, duration_s=175_000, seed=4,
-                      embedded=[Embedding(c, 0.5) for c in chains])
-    types, times = generate_bursty_arrays(cfg)
-    assert 90e6 < len(types) < 110e6
-    rng = np.random.default_rng(44)
-    eps = random_candidates(rng, 2046, 60, 5) + [(c.types, c.constraints) for c in chains]
-    ctx.load_arrays(types, times, 60)
-    got = ctx.count_csr(csr_of(eps))
-    check_subset(types, times, eps, got, 40, 2)
-    tail = csr_of(eps[-2:])
-    want = oracle.count_batch(types, times, tail.offsets, tail.types, tail.low, tail.high, threads=2)
-    np.testing.assert_array_equal(got[-2:], want)
+@pytest.mark.parametrize("kernel", ["chain", "automaton"])
+def test_cfg3_all_candidates(ctx, scale, kernel, monkeypatch):
+    """cfg3: all 10,000 candidates == the reference's count_fsm."""
+    if kernel == "automaton":
+        monkeypatch.setenv("EPI_CHAIN", "0")
+    cell = scale["cfg3"]
+    types, times = stream_of(cell)
+    ctx.load_arrays(types, times, cell["alphabet"])
+    got = ctx.count_csr(cands_of(cell))
+    want = np.array(cell["counts"], np.uint64)
+    bad = np.nonzero(got != want)[0]
+    assert len(bad) == 0, f"{len(bad)} mismatches, first {bad[:5].tolist()}"
+    assert int(got.sum()) == cell["sum"]
+
+
+def test_cfg4_mea_bursty_100m(ctx, scale):
+    """cfg4: the first 1,000 seeded 5-node candidates + the embedded chains
+    over ~100M bursty events == the reference; properties on all of them."""
+    cell = scale["cfg4"]
+    types, times = stream_of(cell)
+    ctx.load_arrays(types, times, cell["alphabet"])
+    csr = cands_of(cell)
+    got = ctx.count_csr(csr)
+    np.testing.assert_array_equal(got, np.array(cell["counts"], np.uint64))
     assert int(got[-1]) > 0 and int(got[-2]) > 0
+    properties(ctx, types, times, cell["alphabet"], csr, got)
 
 
-@pytest.mark.parametrize("n_events,n_cands", [(1_000_000, 1000), (10_000_000, 10000), (100_000_000, 1000)])
-def test_cfg5_sweep_cells(ctx, n_events, n_cands):
-    """cfg5 cells: 64 types at 20 Hz, random 3-node x 3-bin candidates."""
-    duration = n_events / (64 * 20)
-    types, times = generate_arrays(GenConfig(64, duration, 20, [], 5 + n_events))
-    rng = np.random.default_rng(n_events + n_cands)
-    eps = random_candidates(rng, n_cands, 64, 3)
-    ctx.load_arrays(types, times, 64)
-    got = ctx.count_csr(csr_of(eps))
-    check_subset(types, times, eps, got, 24 if n_events >= 100_000_000 else 64, 3)
+@pytest.mark.parametrize("n_events,n_cands", [(1_000_000, 1000), (10_000_000, 10_000), (10_000_000, 1_000_000),
+                                              (100_000_000, 10_000), (1_000_000_000, 1000)])
+def test_cfg5_sweep_cells(ctx, scale, n_events, n_cands):
+    """cfg5 cells: the cell's first 1,000 candidates == the reference; the
+    properties on every candidate of the smaller cells."""
+    name = f"cfg5_{n_events}"
+    if name not in scale:
+        pytest.skip(f"{name} not in the scale fixture")
+    cell = scale[name]
+    types, times = stream_of(cell)
+    ctx.load_arrays(types, times, cell["alphabet"])
+    csr = cands_of(cell, n_cands)
+    got = ctx.count_csr(csr)
+    np.testing.assert_array_equal(got[:1000], np.array(cell["counts"], np.uint64))
+    if n_events * n_cands <= 1e11:
+        properties(ctx, types, times, cell["alphabet"], csr, got)

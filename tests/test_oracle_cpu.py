@@ -126,3 +126,18 @@ def test_port_equals_live_reference_on_fresh_instances():
         for algo in ("fsm", "tracking", "mapconcat"):
             ref = oracle.ref_count_batch(types, times, a, off, et, lo, hi, algo=algo, workers=2)
             np.testing.assert_array_equal(port, ref, err_msg=f"{algo} it {it}")
+
+
+def test_scale_fixture_agrees_with_config_fixture(golden_configs):
+    """tests/golden/scale.json (reference, all 10,000 cfg3 candidates) and
+    configs.json (reference, first 256) were written by separate runs."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "scale.json")) as f:
+        scale = json.load(f)
+    assert scale["cfg3"]["counts"][:256] == golden_configs["cfg3"]["counts"]
+    assert scale["cfg3"]["n"] == golden_configs["cfg3"]["n"]
+    assert len(scale["cfg3"]["counts"]) == 10000
+    for name, cell in scale.items():
+        assert len(cell["counts"]) >= 1000, name
+        assert sum(cell["counts"]) == cell["sum"], name
