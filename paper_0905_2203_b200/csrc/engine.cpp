@@ -33,7 +33,10 @@ enum Slot : size_t {
   kSlotSegments = 6,
   kSlotShardStage = 7,
   kSlotShardCounts = 8,
-  kSlotChainSort = 9,
+  // 10..32 belong to the miner (mine_dev.cu), 40..47 and 140..141 to the
+  // tracking counter (tracking.cu)
+  kSlotChainSort = 60,
+  kSlotChainCounts = 61,
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;
@@ -432,20 +435,33 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // EPI_CHAIN=0 keeps the automaton kernel, EPI_CHAIN=1 uses the chain kernel
   // on sets of any size (tests), EPI_CHAIN_DEPTH=d+1 forces prefix depth d.
   const char* chain_env = std::getenv("EPI_CHAIN");
-  const uint64_t chain_min = chain_env ? (std::atoi(chain_env) == 1 ? 1 : ~0ull) : 1024;
+  const uint64_t chain_min = chain_env ? (std::atoi(chain_env) == 1 ? 1 : ~0ull) : 4096;
   const bool chain = !wide && !ds.last_w && live_slot < 0 && n >= chain_min && p.stages > 0 &&
                      has_chain_kernel(static_cast<int>(N), ds.width, ds.max_high <= 32);
+  // Identical episodes (equal sort keys) are counted once when the set is
+  // large (one synchronisation to size the launch): the kernels count the
+  // distinct ones and a scatter writes every caller slot.
+  ChainSortOut so{};
+  uint64_t* d_final = d_counts;
+  const bool dedup = chain && n >= (std::getenv("EPI_CHAIN") ? 1 : 65536) && !std::getenv("EPI_NO_DEDUP") &&
+                     !capturing_ && !tshard_;
   if (chain) {
     char* sc = scratch_.get<char>(kSlotChainSort, chain_sort_scratch(n, N));
-    ChainSortOut so{};
-    const int own = chain_sort({ds.types, ds.win, ds.sigma, n, N, stream_.alphabet}, sc, so, st_);
+    const int own = chain_sort({ds.types, ds.win, ds.sigma, n, N, stream_.alphabet}, dedup, sc, so, st_);
     stats.kernel_launches += static_cast<uint64_t>(own);
     p.ep_types = so.types;
     p.ep_win = so.win;
     p.ep_sigma = so.sigma;
     p.out_perm = so.perm;
+    if (so.uidx) {
+      // count the distinct episodes into a temporary, scatter afterwards
+      p.n_eps = static_cast<uint32_t>(so.n_unique);
+      p.out_perm = nullptr;
+      p.counts = scratch_.get<uint64_t>(kSlotChainCounts, so.n_unique);
+    }
     if (const char* dd = std::getenv("EPI_CHAIN_DEPTH")) p.chain_depth = std::atoi(dd);
   }
+  const size_t n_launch = p.n_eps;
   auto launch_map = [&]() {
     if (chain) {
       launch_chain(static_cast<int>(N), ds.width, p, st_);
@@ -492,7 +508,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     occ_cache_.emplace_back(shape, bps);
   }
   const int64_t slots = static_cast<int64_t>(num_sms_) * bps;
-  const int64_t ctas_x = (static_cast<int64_t>(n) + 255) / 256;
+  const int64_t ctas_x = (static_cast<int64_t>(n_launch) + 255) / 256;
   const int64_t min_seg = std::max<int64_t>(window_tiles * 4, 32);
   const int64_t max_p = std::clamp<int64_t>(tiles4 / min_seg, 1, kMaxWalkSegments);
   int64_t P = 1;
@@ -559,7 +575,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   p.hist = stream_.d_hist;
   p.matched = d_acc_ + 1;
 
-  const size_t nm = P > 1 ? static_cast<size_t>(ts ? s_rows * tW : P) * n : 1;
+  const size_t nm = P > 1 ? static_cast<size_t>(ts ? s_rows * tW : P) * n_launch : 1;
   const size_t m_count = 0, m_ncomp = align_up(nm * 4, 256), m_last = align_up(m_ncomp + nm * 4, 256),
                m_first = align_up(m_last + nm * 8, 256), m_total = m_first + nm * 8 * kRecorded;
   char* d_mach = scratch_.get<char>(kSlotMachines, m_total);
@@ -579,7 +595,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     const int64_t gq = q * seg_len, gn = std::min<int64_t>((q + 1) * seg_len, tiles4);
     tiles += static_cast<uint64_t>(gn - std::max<int64_t>(gq - window_tiles, 0));
   }
-  Timed t{next_event(), next_event(), nullptr, ms_out, live_slot, n, tiles, true};
+  Timed t{next_event(), next_event(), nullptr, ms_out, live_slot, n_launch, tiles, true};
   rec(t.e0);
   if (ts) {
     p.q_base = static_cast<int32_t>(q0);
@@ -614,6 +630,12 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
       launch_walk_wide(static_cast<int>(N), p, st_);
     else
       launch_walk(static_cast<int>(N), p, st_);
+  }
+  if (so.uidx) {
+    chain_scatter(so, n, p.counts, d_final, st_);
+    stats.kernel_launches += 1;
+  }
+  if (P > 1 || so.uidx) {
     t.e1 = next_event();
     rec(t.e1);
   }

@@ -118,3 +118,21 @@ def test_chain_two_pass_mode(ctx, chain_env):
     keep = got != np.uint64(COUNT_PRUNED)
     np.testing.assert_array_equal(got[keep], want[keep])
     assert np.all(want[~keep] < int(np.median(want)))
+
+
+@pytest.mark.parametrize("dedup", [True, False])
+def test_chain_duplicate_episodes(ctx, chain_env, monkeypatch, dedup):
+    """Identical episodes are counted once (distinct episodes gathered after
+    the sort, counts scattered back to every caller slot); EPI_NO_DEDUP
+    counts every copy."""
+    if not dedup:
+        monkeypatch.setenv("EPI_NO_DEDUP", "1")
+    rng = np.random.default_rng(21)
+    types, times = _stream(rng, 40000, 8, "sparse")
+    ctx.load_arrays(types, times, 8)
+    base = _uniform_batch(rng, 8, 300, 5, 3, 6)
+    eps = [base[int(i)] for i in rng.integers(0, len(base), 5000)]
+    want = port_counts(types, times, base)
+    got = ctx.count_csr(csr_of(eps))
+    index = {(tuple(t), tuple(c)): i for i, (t, c) in enumerate(base)}
+    np.testing.assert_array_equal(got, [want[index[(tuple(t), tuple(c))]] for t, c in eps])
