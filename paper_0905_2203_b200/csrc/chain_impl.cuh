@@ -373,26 +373,26 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
         for (int j = 0; j < nact; j += 4) {
           const uint4 ro = dev::lds_v4(erow_s + j * 4u);
           const uint32_t cg = dev::lds_u32(cgrp_s + j);
-          uint4 dw;
+          uint4 m;
           if (cg != ~0u) {
+            // the 4 episodes share one DD row (the common case: sorted)
             if (cg != cur) {
               cur = cg;
               ddw = in_rng ? dev::lds_u32(dlane_s + cg) : 0u;
             }
-            dw = make_uint4(ddw, ddw, ddw, ddw);
+            m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & ddw) != 0u);
+            m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & ddw) != 0u);
+            m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & ddw) != 0u);
+            m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & ddw) != 0u);
           } else {
             const uint4 go = dev::lds_v4(egrp_s + j * 4u);
-            dw.x = in_rng ? dev::lds_u32(dlane_s + go.x) : 0u;
-            dw.y = in_rng ? dev::lds_u32(dlane_s + go.y) : 0u;
-            dw.z = in_rng ? dev::lds_u32(dlane_s + go.z) : 0u;
-            dw.w = in_rng ? dev::lds_u32(dlane_s + go.w) : 0u;
+            const uint32_t msk = in_rng ? ~0u : 0u;
+            m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & dev::lds_u32(dlane_s + go.x) & msk) != 0u);
+            m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & dev::lds_u32(dlane_s + go.y) & msk) != 0u);
+            m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & dev::lds_u32(dlane_s + go.z) & msk) != 0u);
+            m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & dev::lds_u32(dlane_s + go.w) & msk) != 0u);
             cur = ~0u;
           }
-          uint4 m;
-          m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & dw.x) != 0u);
-          m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & dw.y) != 0u);
-          m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & dw.z) != 0u);
-          m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & dw.w) != 0u);
           if (lane == 0) *reinterpret_cast<uint4*>(&cs.nz[wbase + j]) = m;
         }
         __syncwarp();
