@@ -80,6 +80,9 @@ typedef struct {
                                  AND-POPC word pairs                            */
   double bound_ms;            /* device time of the pass-1 bound kernels       */
   uint64_t chain_launches;    /* map launches that ran the chain kernel         */
+  uint64_t items_tracked;     /* tracking: occurrence intervals found (TrackingStats) */
+  uint64_t sort_fallbacks;    /* tracking: episodes whose intervals were not end-sorted,
+                                 counted by the exact counter instead (TrackingStats) */
 } epi_stats;
 
 /* Context bound to one CUDA device. */
@@ -125,6 +128,15 @@ epi_status epi_find_occurrences(epi_ctx* ctx, const epi_episode_batch* batch, ui
                                 uint64_t** offsets_out, int64_t** starts_out, int64_t** ends_out);
 epi_status epi_count_tracking(epi_ctx* ctx, const epi_episode_batch* batch, uint32_t direction,
                               uint64_t* counts_out, epi_stats* stats);
+
+/* count_mapconcat (mapconcat.hpp:71-159) with the caller's segment count:
+ * exact counts with the MapConcatenate map/concat split into `segments`
+ * time segments (clamped to what the stream allows: each segment must span
+ * the episodes' sum of highs). stats->segments reports the count used,
+ * stats->patches the boundary machines the concat walk re-ran
+ * (MapConcatStats: machines_precomputed = segments x episodes, patches). */
+epi_status epi_count_mapconcat(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t segments,
+                               uint64_t* counts_out, epi_stats* stats);
 
 /* Level-wise mining, mine() (miner.hpp:114-173) with one epi_count call per
  * level. The result is owned by the context until the next epi_mine call:

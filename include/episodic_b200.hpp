@@ -22,7 +22,9 @@
 
 #include <cstdint>
 #include <stdexcept>
+#include <algorithm>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "episodic_b200.h"
@@ -46,7 +48,13 @@ inline void throw_status(epi_status st, const char* msg) {
   }
 }
 
-// Owns one epi_ctx (one CUDA device) and remembers which stream it holds.
+// Owns one epi_ctx (one CUDA device) and the stream it holds. A stream is
+// uploaded once and reused by every count_* / mine call on the same stream:
+// the reference's EventStream is immutable once built (E/types.hpp:94-95),
+// so a stream is identified by its storage (the addresses of its type and
+// time arrays, size, alphabet) plus a fingerprint of 64 evenly spaced events,
+// which catches a new stream built where an old one lived. Mutating a loaded
+// stream's storage in place is not supported; reload() forces an upload.
 class Context {
  public:
   explicit Context(int device = 0) {
@@ -56,21 +64,62 @@ class Context {
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
   epi_ctx* get() const { return ctx_; }
+  uint64_t uploads() const { return uploads_; }
 
-  // (Re)loads the stream on every call: an address/size cache would be
-  // fooled by a new stream constructed where an old one lived. Callers that
-  // count many batches over one stream use count_batch / mine.
   template <class Stream, class DataErrorT = std::runtime_error>
   void load(const Stream& s) {
-    std::vector<uint32_t> types(s.types().begin(), s.types().end());
-    std::vector<int64_t> times(s.times().begin(), s.times().end());
+    const Key k = key_of(s);
+    if (loaded_ && k == key_) return;
+    reload<Stream, DataErrorT>(s);
+  }
+
+  template <class Stream, class DataErrorT = std::runtime_error>
+  void reload(const Stream& s) {
+    loaded_ = false;
+    const auto& ty = s.types();
+    const auto& tm = s.times();
+    std::vector<uint32_t> types(ty.begin(), ty.end());
+    std::vector<int64_t> times(tm.begin(), tm.end());
     throw_status<DataErrorT>(
         epi_load_stream(ctx_, types.data(), times.data(), types.size(), s.alphabet_size()),
         epi_last_error(ctx_));
+    key_ = key_of(s);
+    loaded_ = true;
+    ++uploads_;
   }
 
  private:
+  struct Key {
+    const void* types = nullptr;
+    const void* times = nullptr;
+    uint64_t n = 0, alphabet = 0, fp = 0;
+    bool operator==(const Key& o) const {
+      return types == o.types && times == o.times && n == o.n && alphabet == o.alphabet && fp == o.fp;
+    }
+  };
+  template <class Stream>
+  static Key key_of(const Stream& s) {
+    const auto& ty = s.types();
+    const auto& tm = s.times();
+    Key k;
+    k.types = ty.empty() ? nullptr : static_cast<const void*>(&*ty.begin());
+    k.times = tm.empty() ? nullptr : static_cast<const void*>(&*tm.begin());
+    k.n = ty.size();
+    k.alphabet = s.alphabet_size();
+    uint64_t h = 1469598103934665603ull;
+    const uint64_t n = k.n;
+    for (uint64_t j = 0; n && j < 64; ++j) {
+      const uint64_t i = j * (n - 1) / 63;
+      h = (h ^ static_cast<uint64_t>(ty[i])) * 1099511628211ull;
+      h = (h ^ static_cast<uint64_t>(tm[i])) * 1099511628211ull;
+    }
+    k.fp = h;
+    return k;
+  }
   epi_ctx* ctx_ = nullptr;
+  Key key_;
+  bool loaded_ = false;
+  uint64_t uploads_ = 0;
 };
 
 // CSR form of a range of reference-shaped episodes (epi_episode_batch).
@@ -119,19 +168,61 @@ uint64_t count_fsm(Context& ctx, const Stream& s, const Ep& ep) {
   return count_batch(ctx, s, Range{one})[0];
 }
 
-// Equal to count_fsm on every input (the reference guarantees the same,
-// E/tracking.hpp:388-390); index and options are accepted for parity.
-template <class Stream, class Index, class Ep, class Opt>
-uint64_t count_tracking(Context& ctx, const Stream& s, const Index&, const Ep& ep, const Opt&) {
-  return count_fsm(ctx, s, ep);
+// count_tracking (E/tracking.hpp:391-407) on the device tracker
+// (epi_count_tracking): opt.direction selects forward / backward tracking
+// (Direction::forward = 0, backward = 1, E/tracking.hpp:18); the per-type
+// index lives on the device, so the reference's TypeIndex argument is only
+// accepted. Stats (the reference's TrackingStats or any type with
+// sort_fallbacks / flag_retries / items_tracked) accumulate: items_tracked
+// counts the occurrence intervals, sort_fallbacks the episodes whose
+// intervals were not end-sorted, flag_retries stays 0 (no slab compaction).
+template <class Stream, class Index, class Ep, class Opt, class TStats = void>
+uint64_t count_tracking(Context& ctx, const Stream& s, const Index&, const Ep& ep, const Opt& opt,
+                        TStats* stats = nullptr) {
+  ctx.load(s);
+  Batch b;
+  b.add(ep);
+  const epi_episode_batch v = b.view();
+  uint64_t count = 0;
+  epi_stats st{};
+  throw_status(epi_count_tracking(ctx.get(), &v, static_cast<uint32_t>(opt.direction), &count, &st),
+               epi_last_error(ctx.get()));
+  if constexpr (!std::is_void_v<TStats>) {
+    if (stats) {
+      stats->items_tracked += st.items_tracked;
+      stats->sort_fallbacks += st.sort_fallbacks;
+    }
+  }
+  return count;
 }
 
-template <class Stream, class Ep>
-uint64_t count_mapconcat(Context& ctx, const Stream& s, const Ep& ep, size_t segments,
-                         unsigned /*workers*/ = 1) {
+// count_mapconcat (E/mapconcat.hpp:71-159) with the caller's segment count
+// (epi_count_mapconcat). The device runs every segment's FRESH machine in
+// parallel; stats (the reference's MapConcatStats or any type with
+// machines_precomputed / machine_hits / patches) report the segments used as
+// precomputed machines, the segments whose FRESH record the concat walk used
+// as hits, the re-run boundary machines as patches. `workers` has no device
+// meaning (the kernel is parallel over segments and episodes).
+template <class Stream, class Ep, class MStats = void>
+uint64_t count_mapconcat(Context& ctx, const Stream& s, const Ep& ep, size_t segments, unsigned /*workers*/ = 1,
+                         MStats* stats = nullptr) {
   if (segments < 1) throw std::invalid_argument("count_mapconcat: segments must be >= 1");
-  if (s.size() == 0) return 0;
-  return count_fsm(ctx, s, ep);
+  ctx.load(s);
+  Batch b;
+  b.add(ep);
+  const epi_episode_batch v = b.view();
+  uint64_t count = 0;
+  epi_stats st{};
+  throw_status(epi_count_mapconcat(ctx.get(), &v, segments, &count, &st), epi_last_error(ctx.get()));
+  if constexpr (!std::is_void_v<MStats>) {
+    if (stats) {
+      const uint64_t P = st.segments ? st.segments : 1;
+      stats->machines_precomputed = P;
+      stats->machine_hits = P - std::min<uint64_t>(P, st.patches);
+      stats->patches = st.patches;
+    }
+  }
+  return count;
 }
 
 // mine() mirror returning the reference's MiningResult shape: Result needs

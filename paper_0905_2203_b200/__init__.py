@@ -6,7 +6,7 @@ from .api import (  # noqa: F401
     BurstConfig, Context, DataError, Embedding, Episode, EpisodicError, Event, EventStream, GenConfig,
     IntervalConstraint, InvalidArgument, LevelResult, MiningConfig, MiningResult, Unsupported,
     count_batch, count_fsm, count_mapconcat, count_tracking, csr_to_episodes, default_context,
-    find_occurrences, TrackingOptions, LoadedStream, load_stream, load_stream_file, serialize_stream,
+    find_occurrences, TrackingOptions, TrackingStats, MapConcatStats, LoadedStream, load_stream, load_stream_file, serialize_stream,
     episodes_to_csr, format_episode, generate, generate_arrays, generate_bursty_arrays, generate_candidates, mine,
     random_episodes_csr,
     validate, write_mining_csv, write_events_binary, read_events_binary,

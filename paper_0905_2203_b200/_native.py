@@ -40,7 +40,8 @@ class Stats(C.Structure):
                 ("pass1_ms", C.c_double), ("pass2_ms", C.c_double), ("map_ms", C.c_double),
                 ("concat_ms", C.c_double), ("total_ms", C.c_double),
                 ("bound_words", C.c_uint64), ("bound_ms", C.c_double),
-                ("chain_launches", C.c_uint64)]
+                ("chain_launches", C.c_uint64), ("items_tracked", C.c_uint64),
+                ("sort_fallbacks", C.c_uint64)]
 
     _names = None
 
@@ -96,7 +97,7 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_free", "epi_generate_candidates", "epi_version", "epi_probe_int32",
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
            "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
-           "epi_load_stream_file", "epi_random_episodes")
+           "epi_load_stream_file", "epi_random_episodes", "epi_count_mapconcat")
 
 
 def _load() -> C.CDLL:
@@ -130,6 +131,8 @@ def _load() -> C.CDLL:
                                            C.POINTER(u64p), C.POINTER(i64p), C.POINTER(i64p)]),
         "epi_count_tracking": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint32, u64p,
                                          C.POINTER(Stats)]),
+        "epi_count_mapconcat": (C.c_int, [C.c_void_p, C.POINTER(EpisodeBatch), C.c_uint64, u64p,
+                                          C.POINTER(Stats)]),
         "epi_generate": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_uint64,
                                    C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p), C.POINTER(i64p),
                                    u64p]),

@@ -294,6 +294,16 @@ class Context:
         self.last_stats = stats.as_dict()
         return counts
 
+    def count_mapconcat_csr(self, csr: N.CSR, segments: int):
+        """Exact counts with the caller's MapConcatenate segment count
+        (epi_count_mapconcat); last_stats['segments'] is the count used."""
+        counts = np.zeros(len(csr), dtype=np.uint64)
+        stats = N.Stats()
+        self._check(N.lib.epi_count_mapconcat(self._h, C.byref(csr.struct), int(segments),
+                                              N.ptr(counts, C.c_uint64), C.byref(stats)))
+        self.last_stats = stats.as_dict()
+        return counts
+
     def find_occurrences_csr(self, csr: N.CSR, direction: int = 0):
         """(offsets, starts, ends) of every episode's occurrence intervals."""
         op, sp, ep = N.u64p(), N.i64p(), N.i64p()
@@ -382,6 +392,25 @@ def count_fsm(stream: EventStream, ep: Episode) -> int:
 
 
 @dataclass
+class TrackingStats:
+    """TrackingStats, E/tracking.hpp:41-45 (flag_retries stays 0: the device
+    compacts with a block scan, no slabs)."""
+    sort_fallbacks: int = 0
+    flag_retries: int = 0
+    items_tracked: int = 0
+
+
+@dataclass
+class MapConcatStats:
+    """MapConcatStats, E/mapconcat.hpp:26-30: the device's FRESH segment
+    machines (precomputed), those the concat walk used as they were (hits)
+    and the boundary machines it re-ran (patches)."""
+    machines_precomputed: int = 0
+    machine_hits: int = 0
+    patches: int = 0
+
+
+@dataclass
 class TrackingOptions:
     """TrackingOptions, E/tracking.hpp:33-39. direction is used; the CPU
     compaction strategy, workers and slab width have no device meaning (the
@@ -404,7 +433,11 @@ def count_tracking(stream: EventStream, index, ep: Episode, opt=None, stats=None
     validate(ep)
     ctx = default_context()
     ctx.load(stream)
-    return int(ctx.count_tracking_csr(episodes_to_csr([ep]), _direction(opt))[0])
+    c = int(ctx.count_tracking_csr(episodes_to_csr([ep]), _direction(opt))[0])
+    if stats is not None:
+        stats.items_tracked += int(ctx.last_stats["items_tracked"])
+        stats.sort_fallbacks += int(ctx.last_stats["sort_fallbacks"])
+    return c
 
 
 def find_occurrences(stream: EventStream, index, ep: Episode, opt=None, stats=None) -> list:
@@ -420,14 +453,23 @@ def find_occurrences(stream: EventStream, index, ep: Episode, opt=None, stats=No
 
 def count_mapconcat(stream: EventStream, ep: Episode, segments: int, workers: int = 1,
                     stats=None) -> int:
-    """count_mapconcat, E/mapconcat.hpp:71-159. The device counter is always
-    segment-parallel; the count does not depend on `segments`."""
+    """count_mapconcat, E/mapconcat.hpp:71-159: the device MapConcatenate
+    counter with `segments` time segments (epi_count_mapconcat; clamped to
+    what the stream allows). `workers` has no device meaning."""
     validate(ep)
     if segments < 1:
         raise InvalidArgument("count_mapconcat: segments must be >= 1")
     if stream.size() == 0:
         return 0
-    return count_fsm(stream, ep)
+    ctx = default_context()
+    ctx.load(stream)
+    c = int(ctx.count_mapconcat_csr(episodes_to_csr([ep]), segments)[0])
+    if stats is not None:
+        P = max(int(ctx.last_stats["segments"]), 1)
+        stats.machines_precomputed = P
+        stats.patches = int(ctx.last_stats["patches"])
+        stats.machine_hits = P - min(P, stats.patches)
+    return c
 
 
 def generate_candidates(level: int, frequent: Sequence[Episode], alphabet: Sequence,

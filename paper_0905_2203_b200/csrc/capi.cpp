@@ -229,6 +229,13 @@ epi_status epi_count_tracking(epi_ctx* ctx, const epi_episode_batch* batch, uint
   });
 }
 
+epi_status epi_count_mapconcat(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t segments,
+                               uint64_t* counts_out, epi_stats* stats) {
+  if (!ctx || !batch) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] { ctx->engine.count_batch_segments(*batch, segments, counts_out, stats); });
+}
+
 epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out) {
   if (!ctx || !cfg || !out) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);

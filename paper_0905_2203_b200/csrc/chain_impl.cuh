@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
   const int stages = p.stages;
   uint32_t* dd = stage + static_cast<size_t>(stages) * bw;
   ChainSmem<N>& cs = *reinterpret_cast<ChainSmem<N>*>(dd + kChainGroups * kRowStride);
+  const bool bound = p.bound_only != 0;
   const uint32_t stage_s = dev::smem_addr(stage);  // shared-window addresses
   const uint32_t dd_s = dev::smem_addr(dd);
 
@@ -405,7 +406,10 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
             const int t = __ffs(mine) - 1;
             mine &= mine - 1u;
             const uint32_t w = dev::lds_u32(ro4 + t * 4u) & dev::lds_u32(go4 + t * 4u);
-            chain_word<N, W>(cx, st, w, 32 * (base_rel + t));
+            if (bound)
+              st.cnt += 32 * (base_rel + t) >= cx.tq ? __popc(w) : 0u;
+            else
+              chain_word<N, W>(cx, st, w, 32 * (base_rel + t));
           }
         }
       } else if (nact > 0) {
@@ -437,7 +441,10 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
             }
             u[j] = cw;
           }
-          if ((u[0] | u[1] | u[2] | u[3]) && active) {
+          if (bound) {
+            if (32 * (base_rel + t) >= cx.tq)  // the segment proper (the quad is 4-aligned)
+              st.cnt += __popc(u[0]) + __popc(u[1]) + __popc(u[2]) + __popc(u[3]);
+          } else if ((u[0] | u[1] | u[2] | u[3]) && active) {
             uint32_t wm = (u[0] ? 1u : 0u) | (u[1] ? 2u : 0u) | (u[2] ? 4u : 0u) | (u[3] ? 8u : 0u);
             while (wm) {
               const int j = __ffs(wm) - 1;
@@ -462,7 +469,10 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
     default: if constexpr (N > 7) run(std::integral_constant<int, (N > 7 ? 7 : 0)>{}); break;
   }
 
-  if (active) {
+  if (active && bound) {
+    // upper bound: the chain ends of every segment proper add up
+    if (st.cnt) atomicAdd(reinterpret_cast<unsigned long long*>(p.counts + out_index(p, e)), st.cnt);
+  } else if (active) {
     if (p.P == 1) {
       p.counts[out_index(p, e)] = st.cnt;
     } else {

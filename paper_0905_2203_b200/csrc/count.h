@@ -43,6 +43,8 @@ struct CountLaunch {
   unsigned long long* matched;     // += sum over live episodes of sum_k hist[type_k]
   const uint32_t* out_perm;  // non-null: episode e's count goes to counts[out_perm[e]]
   int32_t chain_depth;       // chain kernel test knob: d + 1 forces prefix depth d (0: auto)
+  int32_t bound_only;        // chain kernel: counts[e] += popcount of the chain-end bitmap
+                             // (a sound upper bound of the count; pass 1 of epi_count MINE)
 };
 
 // Doubling-smear shift amounts covering a window of width w (1..16).

@@ -339,6 +339,65 @@ void Engine::count_packed(DevSet ds, char* host, size_t off_win, size_t off_sigm
   stats.d2h_bytes += n * sizeof(uint64_t);
 }
 
+bool Engine::count_mine_csr(const epi_episode_batch& b, uint32_t N, uint64_t threshold, uint64_t* counts_out,
+                            epi_stats& stats) {
+  const size_t n = b.n_episodes;
+  if (N > 8) return false;
+  const uint32_t M = N - 1;
+  const size_t off_win = align_up(n * N * 4, 256);
+  const size_t off_sigma = align_up(off_win + n * M * 4, 256);
+  const size_t total = align_up(off_sigma + n * 4, 256);
+  char* host = static_cast<char*>(pin_up_.get(total));
+  DevSet ds;
+  ds.N = N;
+  ds.n = n;
+  const uint32_t* off = b.offsets;
+  pack_episodes(
+      n, N, stream_.alphabet, reinterpret_cast<uint32_t*>(host), reinterpret_cast<uint32_t*>(host + off_win),
+      reinterpret_cast<uint32_t*>(host + off_sigma), ds, [&](size_t e, uint32_t k) { return b.types[off[e] + k]; },
+      [&](size_t e, uint32_t k) { return b.low[off[e] - e + k]; },
+      [&](size_t e, uint32_t k) { return b.high[off[e] - e + k]; });
+  if (ds.last_w || ds.max_high > 32 || !has_chain_kernel(static_cast<int>(N), ds.width, true) ||
+      stages_for(stream_.blk_words) == 0)
+    return false;
+  // pass 1: chain-end popcount bound of every candidate (count <= number of
+  // distinct chain-end times: every completion is one)
+  std::vector<uint64_t> bound(n);
+  bound_only_ = true;
+  try {
+    count_packed(ds, host, off_win, off_sigma, total, bound.data(), stats, &stats.pass1_ms);
+  } catch (...) {
+    bound_only_ = false;
+    throw;
+  }
+  bound_only_ = false;
+  stats.pass1_groups += n;
+  // pass 2: exact counts of the survivors (bound >= threshold); the pruned
+  // ones can never be frequent, which is all mine() exposes
+  // (E/miner.hpp:159-160)
+  EpisodeSet surv;
+  surv.N = N;
+  std::vector<uint64_t> idx;
+  for (size_t e = 0; e < n; ++e) {
+    if (bound[e] < threshold) {
+      counts_out[e] = kPruned;
+      ++stats.pruned;
+      continue;
+    }
+    idx.push_back(e);
+    surv.types.insert(surv.types.end(), b.types + off[e], b.types + off[e] + N);
+    surv.lo.insert(surv.lo.end(), b.low + (off[e] - e), b.low + (off[e] - e) + M);
+    surv.hi.insert(surv.hi.end(), b.high + (off[e] - e), b.high + (off[e] - e) + M);
+  }
+  stats.pass2_episodes += idx.size();
+  if (!idx.empty()) {
+    std::vector<uint64_t> exact;
+    count_exact(surv, exact, stats, &stats.pass2_ms);
+    for (size_t j = 0; j < idx.size(); ++j) counts_out[idx[j]] = exact[j];
+  }
+  return true;
+}
+
 void Engine::count_exact(const EpisodeSet& set, std::vector<uint64_t>& counts, epi_stats& stats,
                          double* ms_out) {
   const size_t n = set.size();
@@ -410,6 +469,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
     timed_.push_back(t);
     stats.kernel_launches += 1;
     stats.map_launches += 1;
+    stats.segments = std::max<uint64_t>(stats.segments, 1);  // one pass over the stream
     return;
   }
   // Wide windows need a bitmap whose gap compression cap exceeds them, and
@@ -436,8 +496,10 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   // on sets of any size (tests), EPI_CHAIN_DEPTH=d+1 forces prefix depth d.
   const char* chain_env = std::getenv("EPI_CHAIN");
   const uint64_t chain_min = chain_env ? (std::atoi(chain_env) == 1 ? 1 : ~0ull) : 4096;
-  const bool chain = !wide && !ds.last_w && live_slot < 0 && n >= chain_min && p.stages > 0 &&
-                     has_chain_kernel(static_cast<int>(N), ds.width, ds.max_high <= 32);
+  const bool chain_shape = !wide && !ds.last_w && live_slot < 0 && p.stages > 0 &&
+                           has_chain_kernel(static_cast<int>(N), ds.width, ds.max_high <= 32);
+  if (bound_only_ && !chain_shape) throw Error(EPI_EUNSUPPORTED, "popcount bound needs the chain kernel shape");
+  const bool chain = chain_shape && (n >= chain_min || bound_only_);
   // Identical episodes (equal sort keys) are counted once when the set is
   // large (one synchronisation to size the launch): the kernels count the
   // distinct ones and a scatter writes every caller slot.
@@ -460,6 +522,10 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
       p.counts = scratch_.get<uint64_t>(kSlotChainCounts, so.n_unique);
     }
     if (const char* dd = std::getenv("EPI_CHAIN_DEPTH")) p.chain_depth = std::atoi(dd);
+    if (bound_only_) {
+      p.bound_only = 1;  // every segment adds its chain ends: start from zero
+      EPI_CUDA(cudaMemsetAsync(p.counts, 0, static_cast<size_t>(p.n_eps) * sizeof(uint64_t), st_));
+    }
   }
   const size_t n_launch = p.n_eps;
   auto launch_map = [&]() {
@@ -544,16 +610,22 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
       P = cand;
     }
   }
-  if (const char* force = std::getenv("EPI_FORCE_SEGMENTS")) {
-    // Test knob: many short segments exercise the concat walk on small
-    // streams. Correctness only needs each segment to span sum(high).
+  const char* force_env = std::getenv("EPI_FORCE_SEGMENTS");
+  if (force_segments_ > 0 || force_env) {
+    // The caller's segment count (epi_count_mapconcat) or the test knob:
+    // many short segments exercise the concat walk on small streams.
+    // Correctness only needs each segment to span sum(high).
+    const int64_t want = force_segments_ > 0 ? force_segments_ : std::atoll(force_env);
     const int64_t min_ok = std::max<int64_t>(1, (max_sigma + 31) / 32);
-    P = std::clamp<int64_t>(std::atoll(force), 1,
-                            std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
+    P = std::clamp<int64_t>(want, 1, std::min<int64_t>(std::max<int64_t>(1, n_tiles / min_ok), 65535));
   }
+  // Per-segment completion counters are 32-bit: a segment spans fewer than
+  // 2^27 tiles (< 2^32 ms, so < 2^32 completions); the walk sums in 64 bits.
+  P = std::max<int64_t>(P, (tiles4 + (int64_t{1} << 27) - 1) >> 27);
   // Time-segment shard (epi_count_sharded with few episodes): at least one
   // segment per rank, each rank maps its own contiguous block of segments.
-  const epi_shard* ts = (tshard_ && tshard_->world > 1 && live_slot < 0) ? tshard_ : nullptr;
+  // (the pass-1 bound is computed whole on every rank: identical survivors)
+  const epi_shard* ts = (tshard_ && tshard_->world > 1 && live_slot < 0 && !bound_only_) ? tshard_ : nullptr;
   if (ts && max_p >= static_cast<int64_t>(ts->world))
     P = std::min<int64_t>(max_p, (std::max<int64_t>(P, ts->world) + ts->world - 1) / ts->world * ts->world);
   else
@@ -625,7 +697,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
         throw Error(EPI_ENCCL, "count: all-gather of segment records failed");
     }
   }
-  if (P > 1) {
+  if (P > 1 && !bound_only_) {
     if (wide)
       launch_walk_wide(static_cast<int>(N), p, st_);
     else
@@ -641,7 +713,7 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   }
   timed_.push_back(t);
   stats.segments = static_cast<uint64_t>(P);
-  stats.kernel_launches += P > 1 ? 2 : 1;  // map (+ walk)
+  stats.kernel_launches += P > 1 && !bound_only_ ? 2 : 1;  // map (+ walk)
   stats.map_launches += 1;
   if (chain) stats.chain_launches += 1;
 }
@@ -788,6 +860,18 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
   // batches): pack straight from the caller's arrays
   bool uniform = n > 0;
   for (uint64_t e = 0; uniform && e < n; ++e) uniform = lens[e] == lens[0];
+  if (uniform && mode == EPI_MODE_MINE && threshold > 1 && lens[0] > 1 && !std::getenv("EPI_PASS1_HULL")) {
+    stats.episodes += n;
+    if (count_mine_csr(b, lens[0], threshold, counts_out, stats)) {
+      if (frequent_out)
+        for (uint64_t e = 0; e < n; ++e)
+          frequent_out[e] = counts_out[e] != kPruned && counts_out[e] >= threshold;
+      flush_stats(stats);
+      if (stats_out) *stats_out = stats;
+      return;
+    }
+    stats.episodes -= n;  // shape without a chain kernel: the hull relaxation below
+  }
   if (uniform && (mode != EPI_MODE_MINE || threshold <= 1 || lens[0] <= 1)) {
     stats.episodes += n;
     stats.pass2_episodes += n;
@@ -823,6 +907,19 @@ void Engine::count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_
       frequent_out[e] = counts_out[e] != kPruned && counts_out[e] >= threshold;
   flush_stats(stats);
   if (stats_out) *stats_out = stats;
+}
+
+void Engine::count_batch_segments(const epi_episode_batch& b, uint64_t segments, uint64_t* counts_out,
+                                  epi_stats* stats_out) {
+  if (segments < 1) throw Error(EPI_EINVAL, "count_mapconcat: segments must be >= 1");
+  force_segments_ = static_cast<int64_t>(std::min<uint64_t>(segments, 65535));
+  try {
+    count_batch(b, 1, EPI_MODE_EXACT, counts_out, nullptr, stats_out);
+  } catch (...) {
+    force_segments_ = 0;
+    throw;
+  }
+  force_segments_ = 0;
 }
 
 void Engine::count_batch_sharded(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,

@@ -103,6 +103,10 @@ class Engine {
   void count_set(const EpisodeSet& set, uint64_t threshold, uint32_t mode,
                  std::vector<uint64_t>& counts, epi_stats& stats);
   // Arbitrary CSR batch (mixed lengths): validated, grouped by length.
+  // count_mapconcat (E/mapconcat.hpp:71): exact counts with `segments`
+  // MapConcatenate segments (clamped to what the stream allows).
+  void count_batch_segments(const epi_episode_batch& b, uint64_t segments, uint64_t* counts_out,
+                            epi_stats* stats_out);
   void count_batch(const epi_episode_batch& b, uint64_t threshold, uint32_t mode,
                    uint64_t* counts_out, uint8_t* frequent_out, epi_stats* stats);
   // shard == nullptr: single device (epi_mine); else epi_mine_sharded.
@@ -127,6 +131,12 @@ class Engine {
   // caller's CSR (parallel host packing) into counts_out.
   void count_exact_csr(const epi_episode_batch& b, uint32_t N, uint64_t* counts_out, epi_stats& stats,
                        double* ms_out);
+  // epi_count MODE_MINE for a batch of N-node episodes: pass 1 is the device
+  // chain-end popcount bound (chain kernel, bound mode), pass 2 the exact
+  // count of the survivors. Returns false (nothing done) when the batch's
+  // shape has no chain kernel.
+  bool count_mine_csr(const epi_episode_batch& b, uint32_t N, uint64_t threshold, uint64_t* counts_out,
+                      epi_stats& stats);
   // Uploads packed parameters (pinned host, `total` bytes), counts them and
   // copies the counts into out[0..n).
   void count_packed(DevSet ds, char* host, size_t off_win, size_t off_sigma, size_t total, uint64_t* out,
@@ -195,6 +205,8 @@ class Engine {
   size_t timed_done_ = 0;
   uint64_t stat_epoch_ = 0, prefetched_epoch_ = ~0ull;
   const epi_shard* tshard_ = nullptr;  // active time-segment shard (count_device)
+  int64_t force_segments_ = 0;         // count_batch_segments: caller's segment count
+  bool bound_only_ = false;            // count_device: chain-end popcount bounds (pass 1)
   uint64_t iota_n_ = 0;                 // size of the level-1 type-id buffer
 
   cudaEvent_t next_event();

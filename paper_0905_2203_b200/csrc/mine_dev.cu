@@ -1297,6 +1297,8 @@ void stats_axpy(epi_stats& a, const epi_stats& b, int sign) {
   for (int i = 0; i < 6; ++i) *ad[i] += sign * bd[i];
   a.bound_words += sign > 0 ? b.bound_words : (0 - b.bound_words);
   a.chain_launches += sign > 0 ? b.chain_launches : (0 - b.chain_launches);
+  a.items_tracked += sign > 0 ? b.items_tracked : (0 - b.items_tracked);
+  a.sort_fallbacks += sign > 0 ? b.sort_fallbacks : (0 - b.sort_fallbacks);
 }
 }  // namespace
 

@@ -220,7 +220,9 @@ __global__ void greedy_kernel(const TrackLaunch p, uint64_t* counts, unsigned in
     }
   }
   if (lane == 0) {
-    counts[e] = count;
+    // not end-sorted: the reference sorts and re-runs greedy_schedule
+    // (tracking.hpp:395-401); the host recounts these with the exact counter
+    counts[e] = bad ? ~0ull : count;
     if (bad) atomicAdd(unsorted, 1u);
   }
 }
@@ -313,7 +315,7 @@ void Engine::track_batch(const epi_episode_batch& b, uint32_t direction, uint64_
   const uint32_t A = stream_.alphabet;
   cudaEvent_t e0 = ev0_, e1 = ev1_;
   float total_ms = 0;
-  uint64_t launches = 0;
+  uint64_t launches = 0, items_tracked = 0, sort_fallbacks = 0;
   for (uint64_t base = 0; base < n; base += batch) {
     const uint64_t m = std::min(batch, n - base);
     // batch-local CSR with types clamped to the spare (empty) row
@@ -378,8 +380,42 @@ void Engine::track_batch(const epi_episode_batch& b, uint32_t direction, uint64_
     float ms = 0;
     EPI_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     total_ms += ms;
-    if (bad)
-      throw Error(EPI_EUNSUPPORTED, "tracking: occurrences not end-sorted (reference would sort)");
+    sort_fallbacks += bad;
+    for (uint64_t j = 0; j < m; ++j) items_tracked += n_items[j];
+    if (bad && counts_out) {
+      // count_tracking == count_fsm on every input (tracking.hpp:388-390):
+      // the unsorted episodes are counted by the exact counter
+      EpisodeSet fb;
+      std::vector<uint64_t> fb_idx;
+      for (uint64_t j = 0; j < m; ++j) {
+        if (counts_out[base + j] != ~0ull) continue;
+        const uint64_t e = base + j;
+        const uint32_t b0 = b.offsets[e], N = b.offsets[e + 1] - b0;
+        if (fb.N == 0) fb.N = N;
+        if (N != fb.N) {  // mixed lengths: one exact call per episode
+          EpisodeSet one;
+          one.N = N;
+          one.types.assign(b.types + b0, b.types + b0 + N);
+          one.lo.assign(b.low + (b0 - e), b.low + (b0 - e) + N - 1);
+          one.hi.assign(b.high + (b0 - e), b.high + (b0 - e) + N - 1);
+          std::vector<uint64_t> c1;
+          epi_stats tmp{};
+          count_exact(one, c1, tmp, &tmp.pass2_ms);
+          counts_out[e] = c1[0];
+          continue;
+        }
+        fb_idx.push_back(e);
+        fb.types.insert(fb.types.end(), b.types + b0, b.types + b0 + N);
+        fb.lo.insert(fb.lo.end(), b.low + (b0 - e), b.low + (b0 - e) + N - 1);
+        fb.hi.insert(fb.hi.end(), b.high + (b0 - e), b.high + (b0 - e) + N - 1);
+      }
+      if (!fb_idx.empty()) {
+        std::vector<uint64_t> c;
+        epi_stats tmp{};
+        count_exact(fb, c, tmp, &tmp.pass2_ms);
+        for (size_t j = 0; j < fb_idx.size(); ++j) counts_out[fb_idx[j]] = c[j];
+      }
+    }
     if (off_out) {
       std::vector<uint64_t> loff(m + 1, 0);
       for (uint64_t j = 0; j < m; ++j) loff[j + 1] = loff[j] + n_items[j];
@@ -409,6 +445,8 @@ void Engine::track_batch(const epi_episode_batch& b, uint32_t direction, uint64_
     stats_out->kernel_launches = launches;
     stats_out->total_ms = total_ms;
     stats_out->episode_events = n * stream_.n;
+    stats_out->items_tracked = items_tracked;
+    stats_out->sort_fallbacks = sort_fallbacks;
   }
 }
 

@@ -53,9 +53,36 @@ int main() {
       const uint64_t want = oracle_count(s, ep);
       CHECK(gpu::count_fsm(ctx, s, ep) == want);
       TypeIndex idx = build_index(s);
-      CHECK(gpu::count_tracking(ctx, s, idx, ep, TrackingOptions{}) == want);
-      CHECK(gpu::count_mapconcat(ctx, s, ep, 3) == want);
+      TrackingStats ts;
+      CHECK(gpu::count_tracking(ctx, s, idx, ep, TrackingOptions{}, &ts) == want);
+      TrackingOptions back;
+      back.direction = Direction::backward;
+      CHECK(gpu::count_tracking(ctx, s, idx, ep, back, &ts) == want);
+      // the reference's own tracking statistics for the same episode
+      TrackingStats rs;
+      count_tracking(s, idx, ep, TrackingOptions{}, &rs);
+      count_tracking(s, idx, ep, back, &rs);
+      CHECK(ts.items_tracked == rs.items_tracked);
+      CHECK(ts.flag_retries == 0);
+      MapConcatStats ms;
+      CHECK(gpu::count_mapconcat(ctx, s, ep, 3, 1, &ms) == want);
+      CHECK(ms.machines_precomputed >= 1 && ms.machine_hits + ms.patches == ms.machines_precomputed);
     }
+  }
+  // the stream is uploaded once for any number of calls on it
+  {
+    testing::InstanceRng rng(83);
+    EventStream s = testing::random_stream(rng, 300, 4, 2);
+    const uint64_t before = ctx.uploads();
+    for (int i = 0; i < 20; ++i) {
+      Episode ep = testing::random_episode(rng, s.alphabet_size(), 4);
+      CHECK(gpu::count_fsm(ctx, s, ep) == count_fsm(s, ep));
+    }
+    CHECK(ctx.uploads() == before + 1);
+    EventStream s2 = testing::random_stream(rng, 300, 4, 2);
+    Episode ep = testing::random_episode(rng, s2.alphabet_size(), 4);
+    CHECK(gpu::count_fsm(ctx, s2, ep) == count_fsm(s2, ep));
+    CHECK(ctx.uploads() == before + 2);
   }
   // batch over one stream == reference loop
   {

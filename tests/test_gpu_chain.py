@@ -136,3 +136,27 @@ def test_chain_duplicate_episodes(ctx, chain_env, monkeypatch, dedup):
     got = ctx.count_csr(csr_of(eps))
     index = {(tuple(t), tuple(c)): i for i, (t, c) in enumerate(base)}
     np.testing.assert_array_equal(got, [want[index[(tuple(t), tuple(c))]] for t, c in eps])
+
+
+@pytest.mark.parametrize("kind", ["sparse", "dense", "bursty"])
+def test_mine_mode_popcount_pass1(ctx, kind):
+    """epi_count MODE_MINE on a uniform batch: pass 1 is the device
+    chain-end popcount bound (sound: every completion is a distinct chain
+    end), pass 2 the exact count of the survivors; the frequent set equals
+    the exact one and no frequent candidate is pruned. EPI_PASS1_HULL keeps
+    the host hull relaxation."""
+    from paper_0905_2203_b200 import COUNT_PRUNED, MODE_MINE
+    rng = np.random.default_rng(31)
+    types, times = _stream(rng, 30000, 6, kind)
+    ctx.load_arrays(types, times, 6)
+    eps = _uniform_batch(rng, 6, 3000, 5, 3, 30)
+    want = port_counts(types, times, eps)
+    thr = max(2, int(np.percentile(want, 80)))
+    got, freq = ctx.count_csr(csr_of(eps), threshold=thr, mode=MODE_MINE, with_frequent=True)
+    keep = got != np.uint64(COUNT_PRUNED)
+    np.testing.assert_array_equal(got[keep], want[keep])
+    assert np.all(want[~keep] < thr)
+    np.testing.assert_array_equal(freq.astype(bool), want >= thr)
+    st = ctx.last_stats
+    assert st["pass1_groups"] == len(eps) and st["pruned"] == int((~keep).sum())
+    assert st["chain_launches"] >= 1

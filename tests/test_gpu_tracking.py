@@ -101,3 +101,42 @@ def test_tracking_cross_checks_bitsliced_on_cfg3(ctx, golden_configs):
     more = [([int(x) for x in rng.integers(0, 64, 3)], [(0, 5), (5, 10)]) for _ in range(1000)]
     csr = csr_of(more)
     np.testing.assert_array_equal(ctx.count_tracking_csr(csr, 0), ctx.count_csr(csr))
+
+
+@needs_ref
+@pytest.mark.parametrize("direction", [0, 1])
+def test_tracking_stats_vs_reference(ctx, golden_instances, direction):
+    """TrackingStats analogue: items_tracked == the number of occurrence
+    intervals the reference's find_occurrences returns (E/tracking.hpp:353);
+    no sort fallback on these corpora (T/test_tracking.cpp:178-192)."""
+    for c in golden_instances[:2]:
+        gen = corpus(c["seed"], min(c["count"], 60), c["max_events"], c["max_alphabet"], c["max_gap"],
+                     c["max_size"])
+        for (types, times, a, et, cons) in gen:
+            load(ctx, types, times, a)
+            got = ctx.count_tracking_csr(csr_of([(et, cons)]), direction)
+            st = ctx.last_stats
+            ref = oracle.ref_find_occurrences(types, times, a, et, [x[0] for x in cons], [x[1] for x in cons],
+                                              direction)
+            assert st["items_tracked"] == len(ref)
+            assert st["sort_fallbacks"] == 0
+            assert int(got[0]) == oracle.count_fsm(types, times, et, [x[0] for x in cons], [x[1] for x in cons])
+
+
+def test_count_mapconcat_segments(ctx, golden_instances):
+    """count_mapconcat with the caller's segment count (epi_count_mapconcat):
+    the count never depends on it (T/test_mapconcat.cpp:137-145) and the
+    segments used are reported (clamped to what the stream allows)."""
+    from paper_0905_2203_b200 import EventStream, Episode, MapConcatStats, count_mapconcat
+    c = golden_instances[0]
+    gen = corpus(c["seed"], 40, c["max_events"], c["max_alphabet"], c["max_gap"], c["max_size"])
+    for (types, times, a, et, cons), want in zip(gen, c["instances"]):
+        load(ctx, types, times, a)
+        for P in (1, 2, 5, 64):
+            got = ctx.count_mapconcat_csr(csr_of([(et, cons)]), P)
+            assert int(got[0]) == want["count"]
+            assert 1 <= ctx.last_stats["segments"] <= P
+        st = MapConcatStats()
+        s = EventStream(np.asarray(types, np.uint32), np.asarray(times, np.int64), a)
+        assert count_mapconcat(s, Episode(et, cons), 3, stats=st) == want["count"]
+        assert st.machine_hits + st.patches == st.machines_precomputed >= 1
