@@ -87,6 +87,25 @@ typedef struct {
 
 /* Context bound to one CUDA device. */
 epi_status epi_create(int device, epi_ctx** out);
+
+/* One context over n_gpus devices of this process (SURVEY §8b
+ * "epi_create(int n_gpus, ...)", §8e): one engine and one CUDA stream per
+ * device, the stream replicated on every device, candidates sharded by
+ * episode (few candidates over a long stream: by time segment) with one
+ * all-gather of the u64 counts per level, so a single epi_count / epi_mine
+ * call uses every device (the reference's one-call ThreadPool spread,
+ * E/parallel.hpp:28-125, E/miner.hpp:146-150). devices: n_gpus CUDA ordinals
+ * (NULL: 0 .. n_gpus-1). The exchange is NCCL (libnccl.so.2 loaded at run
+ * time; ncclCommInitAll over the devices) when every device is distinct and
+ * NCCL loads, else device-to-device copies between the ranks' buffers (also
+ * what a group with a repeated device - e.g. several ranks on one GPU for
+ * testing - uses). epi_load_stream / epi_count / epi_mine run on every rank;
+ * the other calls run on the first device. Results and stats come from the
+ * first rank (every rank holds the same counts). */
+epi_status epi_create_multi(int n_gpus, const int* devices, epi_ctx** out);
+/* Ranks of a context (1 for epi_create) and whether its exchange is NCCL. */
+uint32_t epi_world(const epi_ctx* ctx);
+int epi_uses_nccl(const epi_ctx* ctx);
 void epi_destroy(epi_ctx* ctx);
 /* Message of the last failure on ctx (or of the calling thread's last
  * context-free call when ctx is NULL). */

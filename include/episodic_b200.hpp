@@ -60,6 +60,14 @@ class Context {
   explicit Context(int device = 0) {
     throw_status(epi_create(device, &ctx_), epi_last_error(nullptr));
   }
+  // One context over several devices (epi_create_multi): count_batch and
+  // mine spread one call over all of them, as the reference's mine() spreads
+  // one call over its host thread pool (E/parallel.hpp:28-125).
+  explicit Context(const std::vector<int>& devices) {
+    throw_status(epi_create_multi(static_cast<int>(devices.size()), devices.data(), &ctx_),
+                 epi_last_error(nullptr));
+  }
+  uint32_t world() const { return epi_world(ctx_); }
   ~Context() { epi_destroy(ctx_); }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;

@@ -196,16 +196,26 @@ def csr_to_episodes(csr: N.CSR) -> list:
 
 
 class Context:
-    """One device context (epi_ctx): a resident stream plus counting."""
+    """A device context (epi_ctx): a resident stream plus counting.
+    Context(0) binds one device; Context(devices=[0, 1, ...]) one context
+    over several devices of this process (epi_create_multi: stream
+    replicated, candidates sharded, counts all-gathered per level by NCCL or
+    device copies)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices=None):
         h = C.c_void_p()
-        st = N.lib.epi_create(device, C.byref(h))
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+            st = N.lib.epi_create_multi(len(devices), devs, C.byref(h))
+        else:
+            st = N.lib.epi_create(device, C.byref(h))
         if st != N.EPI_OK:
             _raise(st, N.lib.epi_last_error(None).decode())
         self._h = h
         self._loaded = None
-        self.device = device
+        self.device = device if devices is None else int(devices[0])
+        self.world = int(N.lib.epi_world(h))
+        self.uses_nccl = bool(N.lib.epi_uses_nccl(h))
 
     def close(self):
         if getattr(self, "_h", None):

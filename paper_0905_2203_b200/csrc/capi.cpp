@@ -9,12 +9,14 @@
 #include <cstdlib>
 #include <cstring>
 #include <random>
+#include <memory>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "../../include/episodic_b200.h"
 #include "engine.h"
+#include "multi.h"
 
 struct CandStore {
   std::vector<uint32_t> gc_off, gc_types;
@@ -22,8 +24,9 @@ struct CandStore {
 };
 
 struct epi_ctx {
-  epi::Engine engine;
+  epi::Engine engine;  // the (first) device's engine
   CandStore cands;
+  std::unique_ptr<epi::MultiGroup> multi;  // epi_create_multi: every rank
   explicit epi_ctx(int device) : engine(device) {}
 };
 
@@ -161,6 +164,24 @@ epi_status epi_create(int device, epi_ctx** out) {
   return guarded(g_free_err, [&] { *out = new epi_ctx(device); });
 }
 
+epi_status epi_create_multi(int n_gpus, const int* devices, epi_ctx** out) {
+  if (!out || n_gpus < 1) return EPI_EINVAL;
+  *out = nullptr;
+  return guarded(g_free_err, [&] {
+    std::vector<int> devs(static_cast<size_t>(n_gpus));
+    for (int r = 0; r < n_gpus; ++r) devs[r] = devices ? devices[r] : r;
+    std::unique_ptr<epi_ctx> c(new epi_ctx(devs[0]));
+    if (n_gpus > 1) c->multi = std::make_unique<epi::MultiGroup>(c->engine, devs);
+    *out = c.release();
+  });
+}
+
+uint32_t epi_world(const epi_ctx* ctx) {
+  return ctx && ctx->multi ? static_cast<uint32_t>(ctx->multi->world()) : 1u;
+}
+
+int epi_uses_nccl(const epi_ctx* ctx) { return ctx && ctx->multi && ctx->multi->nccl() ? 1 : 0; }
+
 void epi_destroy(epi_ctx* ctx) { delete ctx; }
 
 const char* epi_last_error(const epi_ctx* ctx) {
@@ -171,7 +192,15 @@ epi_status epi_load_stream(epi_ctx* ctx, const uint32_t* types, const int64_t* t
                            uint32_t alphabet) {
   if (!ctx) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);
-  return guarded(ctx->engine.err, [&] { ctx->engine.load_stream_host(types, times, n, alphabet); });
+  return guarded(ctx->engine.err, [&] {
+    if (ctx->multi) {
+      // replicated stream: every device uploads and builds its bitmap
+      ctx->multi->run([&](int r, const epi_shard&) { ctx->multi->rank(r).load_stream_host(types, times, n, alphabet); },
+                      0);
+    } else {
+      ctx->engine.load_stream_host(types, times, n, alphabet);
+    }
+  });
 }
 
 epi_status epi_load_stream_device(epi_ctx* ctx, const uint32_t* d_types, const int64_t* d_times,
@@ -190,7 +219,30 @@ epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t thre
   if (!ctx || !batch) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);
   return guarded(ctx->engine.err, [&] {
-    ctx->engine.count_batch(*batch, threshold, mode, counts_out, frequent_out, stats);
+    if (ctx->multi) {
+      // every rank counts its shard; counts all-gathered, every rank holds all
+      const int G = ctx->multi->world();
+      const uint64_t n = batch->n_episodes;
+      std::vector<std::vector<uint64_t>> c(G);
+      std::vector<std::vector<uint8_t>> f(G);
+      ctx->multi->run(
+          [&](int r, const epi_shard& sh) {
+            uint64_t* co = counts_out;
+            uint8_t* fo = frequent_out;
+            if (r > 0) {
+              c[r].resize(n);
+              co = c[r].data();
+              if (frequent_out) {
+                f[r].resize(n);
+                fo = f[r].data();
+              }
+            }
+            ctx->multi->rank(r).count_batch_sharded(*batch, threshold, mode, sh, co, fo, r == 0 ? stats : nullptr);
+          },
+          4096ull * static_cast<uint64_t>(G));
+    } else {
+      ctx->engine.count_batch(*batch, threshold, mode, counts_out, frequent_out, stats);
+    }
   });
 }
 
@@ -239,7 +291,16 @@ epi_status epi_count_mapconcat(epi_ctx* ctx, const epi_episode_batch* batch, uin
 epi_status epi_mine(epi_ctx* ctx, const epi_mine_config* cfg, epi_mine_result* out) {
   if (!ctx || !cfg || !out) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);
-  return guarded(ctx->engine.err, [&] { ctx->engine.mine(*cfg, out, nullptr); });
+  return guarded(ctx->engine.err, [&] {
+    if (ctx->multi) {
+      // levels of >= 8192 candidates sharded by episode, one all-gather each
+      std::vector<epi_mine_result> res(ctx->multi->world());
+      ctx->multi->run([&](int r, const epi_shard& sh) { ctx->multi->rank(r).mine(*cfg, r == 0 ? out : &res[r], &sh); },
+                      8192);
+    } else {
+      ctx->engine.mine(*cfg, out, nullptr);
+    }
+  });
 }
 
 epi_status epi_count_sharded(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,

@@ -131,6 +131,30 @@ int main() {
       }
     }
   }
+  // one mine() call over a two-rank context (both ranks on device 0 here):
+  // same CSV as the reference
+  {
+    gpu::Context multi(std::vector<int>{0, 0});
+    CHECK(multi.world() == 2);
+    testing::InstanceRng rng(84);
+    EventStream s = testing::random_stream(rng, 3000, 6, 2);
+    MiningConfig c;
+    c.threshold = 5;
+    c.constraint_alphabet = {{0, 5}, {5, 10}};
+    c.max_level = 4;
+    c.workers = 2;
+    MiningResult want = mine(s, c);
+    MiningResult got = gpu::mine<MiningResult>(multi, s, c);
+    std::ostringstream a, b;
+    SymbolTable sym = SymbolTable::numeric(s.alphabet_size());
+    write_mining_csv(a, want, sym);
+    write_mining_csv(b, got, sym);
+    CHECK(a.str() == b.str());
+    std::vector<Episode> eps;
+    for (int i = 0; i < 50; ++i) eps.push_back(testing::random_episode(rng, s.alphabet_size(), 4));
+    std::vector<uint64_t> cnt = gpu::count_batch(multi, s, eps);
+    for (size_t i = 0; i < eps.size(); ++i) CHECK(cnt[i] == count_fsm(s, eps[i]));
+  }
   // exception types of the reference
   {
     EventStream s = testing::stream_of({{0, 1}, {1, 7}}, 2);

@@ -19,7 +19,7 @@ from paper_0905_2203_b200 import (DataError, Embedding, Episode, EpisodicError, 
 def test_library_exports_every_declared_symbol():
     with open(os.path.join(ROOT, "include", "episodic_b200.h")) as f:
         header = f.read()
-    declared = set(re.findall(r"^\s*(?:const char\*|epi_status|void|uint64_t)\s+(epi_\w+)\(", header,
+    declared = set(re.findall(r"^\s*(?:const char\*|epi_status|void|uint64_t|uint32_t|int)\s+(epi_\w+)\(", header,
                               re.M))
     assert "epi_count" in declared and "epi_mine" in declared and len(declared) >= 12
     for name in declared:
