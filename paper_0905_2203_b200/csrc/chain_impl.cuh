@@ -91,7 +91,7 @@ struct ChainCtx {
 
 template <int N, int W>
 __device__ __forceinline__ void chain_record(const ChainCtx<N, W>& x, ChainState& s, int32_t t) {
-  if (s.ncomp < kRecorded) x.first[s.ncomp] = static_cast<uint64_t>(x.T0 + t);
+  if (s.ncomp < kRecorded && x.first) x.first[s.ncomp] = static_cast<uint64_t>(x.T0 + t);
   ++s.ncomp;
   if (t >= x.tq) {
     ++s.cnt;
@@ -278,7 +278,9 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
 #pragma unroll
   for (int k = 0; k < M; ++k) lsum += ep.lo1[k];
   const ChainCtx<N, W> cx{p, ep, T0, g0, gend, 32 * (gq - g0), static_cast<int32_t>(lsum),
-                          p.f_first + (static_cast<size_t>(q) * p.n_eps + e) * kRecorded};
+                          // first completions feed the concat walk only (P > 1)
+                          p.P > 1 && active ? p.f_first + (static_cast<size_t>(q) * p.n_eps + e) * kRecorded
+                                            : nullptr};
   ChainState st;
   {
     const int64_t tqa = static_cast<int64_t>(gq) * 32;

@@ -463,6 +463,9 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
 
   uint32_t cnt = 0, ncomp = 0;
   uint64_t last = ~0ull;
+  // first completions are recorded for the concat walk only (P > 1; with one
+  // segment the record arrays are not allocated per episode)
+  const bool record = active && p.P > 1;
   uint64_t* first = p.f_first + (static_cast<size_t>(q) * p.n_eps + e) * kRecorded;
 
   uint32_t row_off[N];
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kMachThreads) machines_kernel(const CountLaunc
   }
 
   auto on_c = [&](uint64_t tc) -> bool {
-    if (ncomp < kRecorded && active) first[ncomp] = tc;
+    if (ncomp < kRecorded && record) first[ncomp] = tc;
     ++ncomp;
     if (static_cast<int64_t>(tc) >= tq) {
       ++cnt;

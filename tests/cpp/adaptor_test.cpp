@@ -4,6 +4,7 @@
 // container (needs /root/reference headers for the types and checkers);
 // the binary travels to the GPU box and tests/test_cpp_adaptor.py runs it.
 #include <cstdio>
+#include <cstdlib>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -133,7 +134,7 @@ int main() {
   }
   // one mine() call over a two-rank context (both ranks on device 0 here):
   // same CSV as the reference
-  {
+  if (!std::getenv("SKIP_MULTI")) {
     gpu::Context multi(std::vector<int>{0, 0});
     CHECK(multi.world() == 2);
     testing::InstanceRng rng(84);
@@ -144,7 +145,13 @@ int main() {
     c.max_level = 4;
     c.workers = 2;
     MiningResult want = mine(s, c);
+    if (std::getenv("VERBOSE")) {
+      std::fprintf(stderr, "multi mine: %zu events, levels", s.size());
+      for (auto& l : want.levels) std::fprintf(stderr, " %zu", static_cast<size_t>(l.candidates));
+      std::fprintf(stderr, "\n");
+    }
     MiningResult got = gpu::mine<MiningResult>(multi, s, c);
+    if (std::getenv("VERBOSE")) std::fprintf(stderr, "multi mine done\n");
     std::ostringstream a, b;
     SymbolTable sym = SymbolTable::numeric(s.alphabet_size());
     write_mining_csv(a, want, sym);
