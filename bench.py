@@ -286,8 +286,10 @@ def sample_size(name, n_events, steps):
     few seconds of host work at most."""
     if name == "cfg1":
         return 676
-    per_step = max(16, -(-1000 // max(steps, 1)))
-    cap = max(16, int(4e10 // max(n_events, 1)))  # ~1e10-4e10 ee per step
+    cores, _ = cpu_info()
+    # enough episodes per step to keep every host core busy (episode-parallel)
+    per_step = max(4 * cores, -(-1000 // max(steps, 1)))
+    cap = max(2 * cores, int(4e10 // max(n_events, 1)))  # ~1e10-4e10 ee per step
     return min(per_step, cap, 1000)
 
 
@@ -440,7 +442,7 @@ def run_ours(args, rank, world, local_rank):
         e_units = float(ct.item())
     e2e_value = e_units * n / (e_total_ms * 1e-3)
     s0 = e_stats[-1]
-    h2d = n * 12 + int(s0["h2d_bytes"])
+    h2d = ctx.upload_bytes + int(s0["h2d_bytes"])  # the stream as it crossed PCIe + the batch
     d2h = int(s0["d2h_bytes"])
 
     # Roofline of the dominant kernel, per launch, from the engine's CUDA

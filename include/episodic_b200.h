@@ -125,6 +125,11 @@ epi_status epi_load_stream_device(epi_ctx* ctx, const uint32_t* d_types, const i
                                   uint64_t n, uint32_t alphabet);
 
 uint64_t epi_stream_size(const epi_ctx* ctx);
+/* Bytes the last epi_load_stream moved host->device: 12 per event for small
+ * streams; large ones (>= 4M events) cross PCIe encoded - narrowed types,
+ * per-event time deltas against a base every 2048 events, ~2 B/event on the
+ * bench configs - and are widened on the device (ingest.cu). */
+uint64_t epi_stream_upload_bytes(const epi_ctx* ctx);
 
 /* Count every episode of the batch over the loaded stream. counts_out has
  * n_episodes entries; frequent_out (optional) receives count >= threshold.

@@ -98,7 +98,7 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
            "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
            "epi_load_stream_file", "epi_random_episodes", "epi_count_mapconcat", "epi_create_multi",
-           "epi_world", "epi_uses_nccl")
+           "epi_world", "epi_uses_nccl", "epi_stream_upload_bytes")
 
 
 def _load() -> C.CDLL:
@@ -111,6 +111,7 @@ def _load() -> C.CDLL:
         "epi_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
         "epi_create_multi": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
         "epi_world": (C.c_uint32, [C.c_void_p]),
+        "epi_stream_upload_bytes": (C.c_uint64, [C.c_void_p]),
         "epi_uses_nccl": (C.c_int, [C.c_void_p]),
         "epi_destroy": (None, [C.c_void_p]),
         "epi_last_error": (C.c_char_p, [C.c_void_p]),

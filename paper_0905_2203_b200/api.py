@@ -241,6 +241,11 @@ class Context:
                                           stream.alphabet_))
         self._loaded = stream
 
+    @property
+    def upload_bytes(self) -> int:
+        """Host->device bytes of the last stream load (epi_stream_upload_bytes)."""
+        return int(N.lib.epi_stream_upload_bytes(self._h))
+
     def load_arrays(self, types: np.ndarray, times: np.ndarray, alphabet: int):
         """Load from host arrays (pinned or pageable); returns nothing."""
         self._loaded = None

@@ -213,6 +213,14 @@ epi_status epi_load_stream_device(epi_ctx* ctx, const uint32_t* d_types, const i
 
 uint64_t epi_stream_size(const epi_ctx* ctx) { return ctx ? ctx->engine.stream_size() : 0; }
 
+uint64_t epi_stream_upload_bytes(const epi_ctx* ctx) {
+  if (!ctx) return 0;
+  uint64_t b = ctx->engine.last_load_h2d;
+  if (ctx->multi)
+    for (int r = 1; r < ctx->multi->world(); ++r) b += ctx->multi->rank(r).last_load_h2d;
+  return b;
+}
+
 epi_status epi_count(epi_ctx* ctx, const epi_episode_batch* batch, uint64_t threshold,
                      uint32_t mode, uint64_t* counts_out, uint8_t* frequent_out,
                      epi_stats* stats) {

@@ -234,8 +234,16 @@ void Engine::load_stream_host(const uint32_t* types, const int64_t* times, uint6
   if (n && (!types || !times)) throw Error(EPI_EINVAL, "epi_load_stream: null event arrays");
   csr_valid_ = false;
   stream_.reserve_raw(n);
-  h2d(stream_.d_types_raw, types, n * sizeof(uint32_t));
-  h2d(stream_.d_times_raw, times, n * sizeof(int64_t));
+  if (n >= (1ull << 22) && !std::getenv("EPI_RAW_INGEST")) {
+    // large streams cross PCIe narrowed (~2 B/event on the bench configs),
+    // encoded on all host threads while earlier chunks are in flight
+    last_load_h2d = upload_encoded(types, times, n, alphabet, stream_.d_types_raw, stream_.d_times_raw,
+                                   ingest_ring_, st_);
+  } else {
+    h2d(stream_.d_types_raw, types, n * sizeof(uint32_t));
+    h2d(stream_.d_times_raw, times, n * sizeof(int64_t));
+    last_load_h2d = n * 12;
+  }
   stream_.load(n, alphabet, st_, scratch_);
 }
 

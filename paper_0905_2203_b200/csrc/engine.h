@@ -11,6 +11,7 @@
 
 #include "../../include/episodic_b200.h"
 #include "device_stream.h"
+#include "ingest.h"
 
 namespace epi {
 
@@ -279,6 +280,7 @@ class Engine {
   DeviceStream stream_;
   DeviceScratch scratch_;
   PinnedBuffer pin_up_, pin_down_, pin_small_;
+  PinnedRing ingest_ring_;  // compressed stream uploads (ingest.cu)
   MappedBuffer map_out_, map_small_;
 
   // epi_mine result storage

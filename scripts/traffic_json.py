@@ -8,11 +8,17 @@ import sys
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
-out = {}
+# entries whose capture is not in gpurun_out/ keep their committed values
+try:
+    out = json.load(open("profiles/roofline_traffic.json"))
+except (OSError, ValueError):
+    out = {}
 CAPTURES = [
     ("cfg2:machines_kernel", "gpurun_out/prof_cfg2.ncu-rep", "profiles/r01_cfg2_machines_kernel_ncu.txt"),
     ("cfg2:bound_kernel", "gpurun_out/prof_bound.ncu-rep", "profiles/r01_cfg2_bound_kernel_ncu.txt"),
     ("cfg3:machines_kernel", "gpurun_out/prof_cfg3.ncu-rep", "profiles/r01_cfg3_machines_kernel_ncu.txt"),
+    ("cfg5:chain_kernel", "gpurun_out/r02_prof_chain_default.ncu-rep", "profiles/r02_cfg5_chain_kernel_ncu.txt"),
+    ("cfg3:chain_kernel", "gpurun_out/r02_prof_chain_cfg3.ncu-rep", "profiles/r02_cfg3_chain_kernel_ncu.txt"),
 ]
 for cfg, rep, summary in CAPTURES:
     try:

@@ -492,3 +492,48 @@ def test_mine_graph_replay(ctx, golden_configs, monkeypatch):
         # statistics replayed with the graph equal the graph-free run's
         for key in ("pruned", "pass2_episodes", "episodes"):
             assert r2.stats[key] == ref_rel.stats[key], (it, key)
+
+
+@pytest.mark.parametrize("case", ["narrow", "wide_types", "wide_gaps", "huge_gaps"])
+def test_encoded_ingest_matches_raw(ctx, case, monkeypatch):
+    """Streams of >= 4M events cross PCIe encoded (ingest.cu: narrowed types,
+    per-event time deltas against a base every 2048 events); the device SoA
+    they decode to must give the counts of the raw 12 B/event upload."""
+    rng = np.random.default_rng(["narrow", "wide_types", "wide_gaps", "huge_gaps"].index(case))
+    n = 5_000_000
+    a = 300 if case == "wide_types" else 40
+    gmax = {"narrow": 4, "wide_types": 4, "wide_gaps": 5000, "huge_gaps": 1 << 40}[case]
+    gaps = rng.integers(0, 4, n)
+    jumps = rng.random(n) < 1e-4
+    gaps[jumps] = rng.integers(0, gmax, int(jumps.sum()), dtype=np.int64) if gmax > 4 else gaps[jumps]
+    times = np.cumsum(gaps).astype(np.int64)
+    types = rng.integers(0, a, n).astype(np.uint32)
+    eps = [([int(x) for x in rng.integers(0, a, 3)], [BINS[int(b)] for b in rng.integers(0, 3, 2)])
+           for _ in range(300)]
+    csr = csr_of(eps)
+    ctx.load_arrays(types, times, a)
+    got = ctx.count_csr(csr)
+    monkeypatch.setenv("EPI_RAW_INGEST", "1")
+    ctx.load_arrays(types, times, a)
+    np.testing.assert_array_equal(got, ctx.count_csr(csr))
+
+
+@pytest.mark.parametrize("where", [0, 2047, 2048, 262144, 4_999_999])
+def test_encoded_ingest_reports_first_offender(ctx, where):
+    """A chunk holding an invalid event ships raw, so the device validation
+    reports the reference's message (E/types.hpp:109-111) on the encoded path
+    as on the raw one."""
+    n = 5_000_000
+    types = (np.arange(n) % 7).astype(np.uint32)
+    times = np.arange(n, dtype=np.int64)
+    for kind in ("regress", "negative", "type"):
+        t, tm = types.copy(), times.copy()
+        if kind == "regress" and where > 0:
+            tm[where] = tm[where - 1] - 1
+        elif kind == "negative" or (kind == "regress" and where == 0):
+            tm[: where + 1] -= where + 5
+        else:
+            t[where] = 9
+        want = {"regress": "non-decreasing", "negative": "negative event time", "type": "out of range"}[kind]
+        with pytest.raises(DataError, match=want if not (kind == "regress" and where == 0) else "negative"):
+            ctx.load_arrays(t, tm, 7)
