@@ -242,6 +242,17 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
                         uint32_t** types_out, int64_t** times_out, uint64_t* n_out);
 void epi_free(void* p);
 
+/* generate() bit-exact ON THE DEVICE, straight into the context's stream
+ * (as if its arrays were passed to epi_load_stream): one
+ * CTA per neuron runs the neuron's mt19937_64 stream and accumulates its
+ * spike times in the reference's order, the embedded episodes are generated
+ * on the host (few events), one device radix sort merges them. A 1B-event
+ * stream takes a fraction of a second instead of host minutes. */
+epi_status epi_generate_stream(epi_ctx* ctx, uint32_t neurons, double duration_s, double base_rate_hz,
+                               uint64_t seed, const epi_episode_batch* embedded, const double* rates);
+/* Copies the loaded stream (epi_stream_size events) to host arrays. */
+epi_status epi_stream_download(epi_ctx* ctx, uint32_t* types_out, int64_t* times_out);
+
 /* Event-file ingest, load_stream (io.hpp:22-56) restated multi-threaded:
  * `<name>,<int_ms>` per line, '#' comments and blank lines skipped, CRLF
  * tolerated. Type ids are the names' first-seen order; *names_out receives

@@ -98,7 +98,8 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_generate_bursty", "epi_find_occurrences", "epi_count_tracking", "epi_parse_events",
            "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
            "epi_load_stream_file", "epi_random_episodes", "epi_count_mapconcat", "epi_create_multi",
-           "epi_world", "epi_uses_nccl", "epi_stream_upload_bytes")
+           "epi_world", "epi_uses_nccl", "epi_stream_upload_bytes", "epi_generate_stream",
+           "epi_stream_download")
 
 
 def _load() -> C.CDLL:
@@ -142,6 +143,9 @@ def _load() -> C.CDLL:
                                    C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p), C.POINTER(i64p),
                                    u64p]),
         "epi_free": (None, [C.c_void_p]),
+        "epi_generate_stream": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_double, C.c_uint64,
+                                          C.POINTER(EpisodeBatch), f64p]),
+        "epi_stream_download": (C.c_int, [C.c_void_p, u32p, i64p]),
         "epi_generate_bursty": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_double,
                                           C.c_double, C.c_double, C.c_double, C.c_uint64,
                                           C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p),

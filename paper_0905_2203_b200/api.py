@@ -241,6 +241,26 @@ class Context:
                                           stream.alphabet_))
         self._loaded = stream
 
+    def generate(self, cfg: "GenConfig"):
+        """generate() (E/datagen.hpp:71-122) bit-exact on the device, loaded as
+        this context's stream (epi_generate_stream)."""
+        eps = [e.episode for e in cfg.embedded]
+        csr = episodes_to_csr(eps) if eps else None
+        rates = np.array([e.rate_hz for e in cfg.embedded], dtype=np.float64)
+        self._loaded = None
+        self._check(N.lib.epi_generate_stream(self._h, int(cfg.neurons), float(cfg.duration_s),
+                                              float(cfg.base_rate_hz), int(cfg.seed) & ((1 << 64) - 1),
+                                              C.byref(csr.struct) if csr is not None else None,
+                                              N.ptr(rates, C.c_double) if len(rates) else None))
+
+    def download(self):
+        """(types, times) of the loaded stream (epi_stream_download)."""
+        n = int(N.lib.epi_stream_size(self._h))
+        types = np.zeros(n, dtype=np.uint32)
+        times = np.zeros(n, dtype=np.int64)
+        self._check(N.lib.epi_stream_download(self._h, N.ptr(types, C.c_uint32), N.ptr(times, C.c_int64)))
+        return types, times
+
     @property
     def upload_bytes(self) -> int:
         """Host->device bytes of the last stream load (epi_stream_upload_bytes)."""

@@ -342,6 +342,28 @@ epi_status epi_generate(uint32_t neurons, double duration_s, double base_rate_hz
 
 void epi_free(void* p) { std::free(p); }
 
+epi_status epi_generate_stream(epi_ctx* ctx, uint32_t neurons, double duration_s, double base_rate_hz,
+                               uint64_t seed, const epi_episode_batch* embedded, const double* rates) {
+  if (!ctx) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    if (ctx->multi)
+      ctx->multi->run(
+          [&](int r, const epi_shard&) {
+            ctx->multi->rank(r).generate_stream_device(neurons, duration_s, base_rate_hz, seed, embedded, rates);
+          },
+          0);
+    else
+      ctx->engine.generate_stream_device(neurons, duration_s, base_rate_hz, seed, embedded, rates);
+  });
+}
+
+epi_status epi_stream_download(epi_ctx* ctx, uint32_t* types_out, int64_t* times_out) {
+  if (!ctx) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] { ctx->engine.download_stream(types_out, times_out); });
+}
+
 epi_status epi_parse_events(const char* text, uint64_t len, uint32_t** types_out,
                             int64_t** times_out, uint64_t* n_out, char** names_out,
                             uint32_t* alphabet_out) {

@@ -170,6 +170,34 @@ void generate_stream(uint32_t neurons, double duration_s, double base_rate_hz, u
   }
 }
 
+// The embedded-episode events of generate() alone (E/datagen.hpp:100-115),
+// unsorted, after the same validation: the device generator (gen_dev.cu)
+// produces the neurons' Poisson background and merges these in.
+void generate_embedded_events(uint32_t neurons, double duration_s, uint64_t seed, const epi_episode_batch* emb,
+                              const double* rates, std::vector<uint32_t>& types, std::vector<int64_t>& times) {
+  validate_embedded(neurons, emb, rates);
+  types.clear();
+  times.clear();
+  const uint64_t ne = emb ? emb->n_episodes : 0;
+  for (uint64_t e = 0; e < ne; ++e) {
+    const uint32_t b0 = emb->offsets[e], N = emb->offsets[e + 1] - b0;
+    const uint64_t cb = b0 - e;
+    Rng rng(splitmix64(seed ^ (0xE1BEDDEDULL + (e << 20))));
+    double start_s = rng.exponential(rates[e]);
+    while (start_s < duration_s) {
+      int64_t t = static_cast<int64_t>(start_s * 1000.0);
+      types.push_back(emb->types[b0]);
+      times.push_back(t);
+      for (uint32_t k = 1; k < N; ++k) {
+        t += rng.uniform_gap(emb->low[cb + k - 1], emb->high[cb + k - 1]);
+        types.push_back(emb->types[b0 + k]);
+        times.push_back(t);
+      }
+      start_s += rng.exponential(rates[e]);
+    }
+  }
+}
+
 // MEA-culture-shaped bursty generator (the reference
 // generator has no burst model, E/datagen.hpp:91-98). Deterministic under a
 // seed, with the reference's Rng (mt19937_64 raw output + splitmix64 seeds):

@@ -37,6 +37,7 @@ enum Slot : size_t {
   // tracking counter (tracking.cu)
   kSlotChainSort = 60,
   kSlotChainCounts = 61,
+  // 62: the device generator's keys and sort buffers (gen_dev.cu)
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;
@@ -245,6 +246,16 @@ void Engine::load_stream_host(const uint32_t* types, const int64_t* times, uint6
     last_load_h2d = n * 12;
   }
   stream_.load(n, alphabet, st_, scratch_);
+}
+
+void Engine::download_stream(uint32_t* types, int64_t* times) {
+  require_stream();
+  const uint64_t n = stream_.n;
+  if (n == 0) return;
+  if (!types || !times) throw Error(EPI_EINVAL, "epi_stream_download: null arrays");
+  EPI_CUDA(cudaMemcpyAsync(types, stream_.d_types_raw, n * 4, cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaMemcpyAsync(times, stream_.d_times_raw, n * 8, cudaMemcpyDeviceToHost, st_));
+  EPI_CUDA(cudaStreamSynchronize(st_));
 }
 
 void Engine::load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,

@@ -92,6 +92,12 @@ class Engine {
   ~Engine();
 
   void load_stream_host(const uint32_t* types, const int64_t* times, uint64_t n, uint32_t alphabet);
+  // generate() (E/datagen.hpp:71-122) bit-exact on the device, loaded as the
+  // context's stream (gen_dev.cu).
+  void generate_stream_device(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
+                              const epi_episode_batch* emb, const double* rates);
+  // Copies the loaded stream's SoA back to host arrays (stream_size entries).
+  void download_stream(uint32_t* types, int64_t* times);
   void load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,
                           uint32_t alphabet);
   uint64_t stream_size() const { return stream_.n; }
