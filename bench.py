@@ -322,10 +322,20 @@ def run_ours(args, rank, world, local_rank):
     # collectives on device tensors for NCCL; gloo (EPI_BENCH_BACKEND, for
     # functional runs with several ranks on one GPU) takes host tensors
     coll_dev = dev if os.environ.get("EPI_BENCH_BACKEND", "nccl") == "nccl" else None
-    types, times, alphabet = make_stream(args.config, args.cfg5_events)
-    n = len(types)
     ctx = Context(gpu)
-    ctx.load_arrays(types, times, alphabet)
+    sp = stream_spec(args.config, args.cfg5_events)
+    if sp["kind"] == "generate":
+        # the reference's generate() run bit-exact on the device
+        # (epi_generate_stream); the host copy feeds the end-to-end leg
+        from paper_0905_2203_b200 import Embedding, Episode, GenConfig
+        ctx.generate(GenConfig(sp["neurons"], sp["duration_s"], sp["rate_hz"],
+                               [Embedding(Episode(t, c), r) for t, c, r in sp["embedded"]], sp["seed"]))
+        types, times = ctx.download()
+        alphabet = alphabet_of(sp)
+    else:
+        types, times, alphabet = make_stream(args.config, args.cfg5_events)
+        ctx.load_arrays(types, times, alphabet)
+    n = len(types)
 
     # Pinned host copies for the end-to-end leg.
     h_types = torch.from_numpy(types).pin_memory()

@@ -54,11 +54,9 @@ struct ChainSmem {
   uint32_t edge[8][2 * N];          // last lane of each warp: its episode (prefix compare)
   uint32_t wheads[8];
   // row mode: per episode the byte offset of its last type's row in a staged
-  // block and of its group's DD row; per chunk of 4 episodes the DD row
-  // offset when they share one group (~0u otherwise); the per-block ballots
+  // block and of its group's DD row; the per-block ballots
   __align__(16) uint32_t erow[kMachThreads];
   __align__(16) uint32_t egrp[kMachThreads];
-  __align__(16) uint32_t cgrp[kMachThreads / 4];
   __align__(16) uint32_t nz[kMachThreads];
 };
 
@@ -266,10 +264,6 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
     const uint32_t eg = static_cast<uint32_t>(grp > 0 ? grp : 0) * kRowStride * 4u;
     cs.erow[tid] = ep.type[N - 1] * kRowStride * 4u;
     cs.egrp[tid] = eg;
-    // chunk of 4 consecutive episodes with one group: lanes 4i..4i+3 agree
-    const uint32_t g0c = __shfl_sync(0xffffffffu, eg, lane & ~3);
-    const bool agree = ((__ballot_sync(0xffffffffu, eg != g0c) >> (lane & ~3)) & 15u) == 0;
-    if ((lane & 3) == 0) cs.cgrp[tid >> 2] = agree ? eg : ~0u;
   }
 
   // ---- per-segment greedy state ---------------------------------------------
@@ -371,31 +365,16 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
         const bool in_rng = lane >= t0 && lane < t1;
         const uint32_t lane_s = sbase_s + lane * 4u, dlane_s = dd_s + lane * 4u;
         const uint32_t erow_s = dev::smem_addr(&cs.erow[wbase]), egrp_s = dev::smem_addr(&cs.egrp[wbase]);
-        const uint32_t cgrp_s = dev::smem_addr(&cs.cgrp[wbase >> 2]);
-        uint32_t cur = ~0u, ddw = 0;
+        // (lanes outside [t0, t1) read word 0 of the rows, masked away)
+        const uint32_t msk = in_rng ? ~0u : 0u;
         for (int j = 0; j < nact; j += 4) {
           const uint4 ro = dev::lds_v4(erow_s + j * 4u);
-          const uint32_t cg = dev::lds_u32(cgrp_s + j);
+          const uint4 go = dev::lds_v4(egrp_s + j * 4u);
           uint4 m;
-          if (cg != ~0u) {
-            // the 4 episodes share one DD row (the common case: sorted)
-            if (cg != cur) {
-              cur = cg;
-              ddw = in_rng ? dev::lds_u32(dlane_s + cg) : 0u;
-            }
-            m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & ddw) != 0u);
-            m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & ddw) != 0u);
-            m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & ddw) != 0u);
-            m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & ddw) != 0u);
-          } else {
-            const uint4 go = dev::lds_v4(egrp_s + j * 4u);
-            const uint32_t msk = in_rng ? ~0u : 0u;
-            m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & dev::lds_u32(dlane_s + go.x) & msk) != 0u);
-            m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & dev::lds_u32(dlane_s + go.y) & msk) != 0u);
-            m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & dev::lds_u32(dlane_s + go.z) & msk) != 0u);
-            m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & dev::lds_u32(dlane_s + go.w) & msk) != 0u);
-            cur = ~0u;
-          }
+          m.x = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.x) & dev::lds_u32(dlane_s + go.x) & msk) != 0u);
+          m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & dev::lds_u32(dlane_s + go.y) & msk) != 0u);
+          m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & dev::lds_u32(dlane_s + go.z) & msk) != 0u);
+          m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & dev::lds_u32(dlane_s + go.w) & msk) != 0u);
           if (lane == 0) *reinterpret_cast<uint4*>(&cs.nz[wbase + j]) = m;
         }
         __syncwarp();

@@ -39,9 +39,13 @@ def scale():
         return json.load(f)
 
 
-def stream_of(cell):
+def stream_of(cell, ctx=None):
     s = cell["stream"]
-    if s["kind"] == "generate":
+    if s["kind"] == "generate" and ctx is not None:
+        # the device generator (bit-exact generate(); tests/test_gpu_datagen.py)
+        ctx.generate(GenConfig(s["neurons"], s["duration_s"], s["rate_hz"], [], s["seed"]))
+        types, times = ctx.download()
+    elif s["kind"] == "generate":
         types, times = generate_arrays(GenConfig(s["neurons"], s["duration_s"], s["rate_hz"], [], s["seed"]))
     else:
         emb = [Embedding(Episode(t, [tuple(c) for c in cs]), s["embedded_rate_hz"]) for t, cs in cell["extra"]]
@@ -130,8 +134,7 @@ def test_cfg5_sweep_cells(ctx, scale, n_events, n_cands):
     if name not in scale:
         pytest.skip(f"{name} not in the scale fixture")
     cell = scale[name]
-    types, times = stream_of(cell)
-    ctx.load_arrays(types, times, cell["alphabet"])
+    types, times = stream_of(cell, ctx)  # generated on the device, already loaded
     csr = cands_of(cell, n_cands)
     got = ctx.count_csr(csr)
     np.testing.assert_array_equal(got[:1000], np.array(cell["counts"], np.uint64))
