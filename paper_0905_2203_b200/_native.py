@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libepisodic_b200.so")
+# EPI_LIB: an alternative in-tree build of the library (kernel experiments)
+LIB_PATH = os.environ.get("EPI_LIB") or os.path.join(_HERE, "_lib", "libepisodic_b200.so")
 
 EPI_OK, EPI_EINVAL, EPI_EDATA, EPI_EOVERFLOW, EPI_ECUDA, EPI_ENCCL, EPI_ENOMEM, EPI_EUNSUPPORTED = range(8)
 MODE_EXACT, MODE_MINE = 0, 1

@@ -399,41 +399,73 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
 #pragma unroll
         for (int k = 0; k < N; ++k) ra[k] = sbase_s + ep.type[k] * kRowStride * 4u + t0 * 4u;
         uint32_t da = dd_s + grow4 + t0 * 4u;
-        for (int32_t t = t0; t < t1; t += 4) {
-          uint4 v[N];
+        // chain-end words are queued (two per lane, in time order) and taken
+        // through the greedy after the block, when every lane's queue is
+        // drained together instead of once per lane that has a chain end
+        uint32_t qw0 = 0, qw1 = 0;
+        int32_t qt0 = 0, qt1 = 0;
+        int qn = 0;
+        auto quads = [&](auto btag) {
+          constexpr bool kBound = decltype(btag)::value;
+          for (int32_t t = t0; t < t1; t += 4) {
+            uint4 v[N];
 #pragma unroll
-          for (int k = D; k < N; ++k) v[k] = dev::lds_v4(ra[k]);
-          uint4 dv = make_uint4(0, 0, 0, 0);
-          if constexpr (D > 0) dv = dev::lds_v4(da);
+            for (int k = D; k < N; ++k) v[k] = dev::lds_v4(ra[k]);
+            uint4 dv = make_uint4(0, 0, 0, 0);
+            if constexpr (D > 0) dv = dev::lds_v4(da);
 #pragma unroll
-          for (int k = 0; k < N; ++k) ra[k] += 16u;
-          da += 16u;
-          uint32_t u[4];
+            for (int k = D; k < N; ++k) ra[k] += 16u;
+            da += 16u;
+            uint32_t u[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            auto pick = [&](const uint4& a) { return j == 0 ? a.x : j == 1 ? a.y : j == 2 ? a.z : a.w; };
-            uint32_t cw = D > 0 ? (pick(v[D]) & pick(dv)) : pick(v[0]);
+            for (int j = 0; j < 4; ++j) {
+              auto pick = [&](const uint4& a) { return j == 0 ? a.x : j == 1 ? a.y : j == 2 ? a.z : a.w; };
+              uint32_t cw = D > 0 ? (pick(v[D]) & pick(dv)) : pick(v[0]);
 #pragma unroll
-            for (int k = D + 1; k < N; ++k) {
-              const uint32_t hi = ep.hi[k - 1];
-              const uint32_t nx = pick(v[k]) & window_any<W, true>(cw, h[k - 1], 0u, hi - W + 1, hi);
-              h[k - 1] = cw;
-              cw = nx;
+              for (int k = D + 1; k < N; ++k) {
+                const uint32_t hi = ep.hi[k - 1];
+                const uint32_t nx = pick(v[k]) & window_any<W, true>(cw, h[k - 1], 0u, hi - W + 1, hi);
+                h[k - 1] = cw;
+                cw = nx;
+              }
+              u[j] = cw;
             }
-            u[j] = cw;
-          }
-          if (bound) {
-            if (32 * (base_rel + t) >= cx.tq)  // the segment proper (the quad is 4-aligned)
-              st.cnt += __popc(u[0]) + __popc(u[1]) + __popc(u[2]) + __popc(u[3]);
-          } else if ((u[0] | u[1] | u[2] | u[3]) && active) {
-            uint32_t wm = (u[0] ? 1u : 0u) | (u[1] ? 2u : 0u) | (u[2] ? 4u : 0u) | (u[3] ? 8u : 0u);
-            while (wm) {
-              const int j = __ffs(wm) - 1;
-              wm &= wm - 1u;
-              const uint32_t w = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
-              chain_word<N, W>(cx, st, w, 32 * (base_rel + t + j));
+            if constexpr (kBound) {
+              if (32 * (base_rel + t) >= cx.tq)  // the segment proper (the quad is 4-aligned)
+                st.cnt += __popc(u[0]) + __popc(u[1]) + __popc(u[2]) + __popc(u[3]);
+            } else if ((u[0] | u[1] | u[2] | u[3]) && active) {
+              uint32_t wm = (u[0] ? 1u : 0u) | (u[1] ? 2u : 0u) | (u[2] ? 4u : 0u) | (u[3] ? 8u : 0u);
+              while (wm) {
+                const int j = __ffs(wm) - 1;
+                wm &= wm - 1u;
+                const uint32_t w = j == 0 ? u[0] : j == 1 ? u[1] : j == 2 ? u[2] : u[3];
+                const int32_t base = 32 * (base_rel + t + j);
+                if (qn == 0) {
+                  qw0 = w;
+                  qt0 = base;
+                  qn = 1;
+                } else if (qn == 1) {
+                  qw1 = w;
+                  qt1 = base;
+                  qn = 2;
+                } else {
+                  // queue full (dense streams): drain it, then this word
+                  chain_word<N, W>(cx, st, qw0, qt0);
+                  chain_word<N, W>(cx, st, qw1, qt1);
+                  chain_word<N, W>(cx, st, w, base);
+                  qn = 0;
+                }
+              }
             }
           }
+        };
+        if (bound)
+          quads(std::true_type{});
+        else
+          quads(std::false_type{});
+        if (qn > 0) {
+          chain_word<N, W>(cx, st, qw0, qt0);
+          if (qn > 1) chain_word<N, W>(cx, st, qw1, qt1);
         }
       }
       __syncthreads();  // stage slot and DD rows free for reuse
