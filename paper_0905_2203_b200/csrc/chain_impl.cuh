@@ -42,7 +42,7 @@
 namespace epi {
 namespace impl {
 
-constexpr int kChainGroups = 64;  // max shared prefixes per CTA (phase A rows)
+constexpr int kChainGroups = 32;  // max shared prefixes per CTA (phase A rows)
 constexpr int kChainMaxN = 8;
 
 template <int N>
@@ -57,13 +57,13 @@ struct ChainSmem {
   // block and of its group's DD row; the per-block ballots
   __align__(16) uint32_t erow[kMachThreads];
   __align__(16) uint32_t egrp[kMachThreads];
-  __align__(16) uint32_t nz[kMachThreads];
+  __align__(16) uint32_t nz[2][kMachThreads];
 };
 
 inline size_t chain_smem(const CountLaunch& p) {
   // bars + stage ring + DD rows + ChainSmem<N> (bounded by N = kChainMaxN)
   return 128 + static_cast<size_t>(p.stages) * p.blk_words * 4 +
-         static_cast<size_t>(kChainGroups) * kRowStride * 4 + sizeof(ChainSmem<kChainMaxN>);
+         2 * static_cast<size_t>(kChainGroups) * kRowStride * 4 + sizeof(ChainSmem<kChainMaxN>);
 }
 
 // Greedy state of one (episode, segment) machine, times relative to
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
   const uint32_t bw = p.blk_words;
   const int stages = p.stages;
   uint32_t* dd = stage + static_cast<size_t>(stages) * bw;
-  ChainSmem<N>& cs = *reinterpret_cast<ChainSmem<N>*>(dd + kChainGroups * kRowStride);
+  ChainSmem<N>& cs = *reinterpret_cast<ChainSmem<N>*>(dd + 2 * kChainGroups * kRowStride);
   const bool bound = p.bound_only != 0;
   const uint32_t stage_s = dev::smem_addr(stage);  // shared-window addresses
   const uint32_t dd_s = dev::smem_addr(dd);
@@ -300,16 +300,21 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
     dev::bulk_g2s(stage + static_cast<size_t>(c % stages) * bw, p.occ + static_cast<size_t>(blk0 + c) * bw,
                   bw * 4u, bar);
   };
+  // Row mode with >= 4 stages takes two bitmap blocks per iteration (half the
+  // per-block bookkeeping, one row-table read per two blocks): the ring then
+  // runs stages - 2 blocks ahead.
+  const bool pair = dsel == M && stages >= 4;
+  const int ahead = pair ? stages - 2 : stages - 1;
   __syncthreads();  // group table written; barriers initialised
   if (tid == 0)
-    for (int32_t c = 0; c < stages - 1 && c < nblk; ++c) issue(c);
+    for (int32_t c = 0; c < ahead && c < nblk; ++c) issue(c);
   // episodes of this warp (row mode walks them with lane = tile)
   const int wbase = warp * 32;
   const int nact = static_cast<int>(n_live) - (static_cast<int>(eblk) * kMachThreads + wbase) < 32
                        ? max(0, static_cast<int>(n_live) - (static_cast<int>(eblk) * kMachThreads + wbase))
                        : 32;
 
-  auto phase_a = [&](auto dtag, uint32_t sbase_s, int32_t t0) {
+  auto phase_a = [&](auto dtag, uint32_t sbase_s, int32_t t0, uint32_t* ddw) {
     constexpr int D = decltype(dtag)::value;
     for (int gi = warp; gi < G; gi += kMachThreads / 32) {
       const bool live = lane >= t0;
@@ -328,7 +333,7 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
       uint32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
       if (lane == 0) prev = cs.carry[gi][D - 1];
       const uint32_t hi = cs.ghi[gi][D - 1];
-      dd[gi * kRowStride + lane] = window_any<W, true>(x, prev, 0u, hi - W + 1, hi);
+      ddw[gi * kRowStride + lane] = window_any<W, true>(x, prev, 0u, hi - W + 1, hi);
       __syncwarp();
       if (lane == 31) {
 #pragma unroll
@@ -346,15 +351,86 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
     for (int k = 0; k < M; ++k) h[k] = 0;
     const uint32_t grow4 = static_cast<uint32_t>(grp > 0 ? grp : 0) * kRowStride * 4u;
 
+    if constexpr (D == M) {
+      if (pair) {
+        const uint32_t erow_s = dev::smem_addr(&cs.erow[wbase]), egrp_s = dev::smem_addr(&cs.egrp[wbase]);
+        for (int32_t c = 0; c < nblk; c += 2) {
+          const bool two = c + 1 < nblk;
+          if (tid == 0) {
+            if (c + ahead < nblk) issue(c + ahead);
+            if (c + ahead + 1 < nblk) issue(c + ahead + 1);
+          }
+          int32_t gbs[2], t0s[2], t1s[2];
+          uint32_t sb[2];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int32_t cb = two ? c + b : c;
+            gbs[b] = (blk0 + cb) * 32;
+            t0s[b] = g0 > gbs[b] ? g0 - gbs[b] : 0;
+            t1s[b] = gend - gbs[b] < 32 ? gend - gbs[b] : 32;
+            sb[b] = stage_s + static_cast<uint32_t>(cb % stages) * bw * 4u;
+          }
+          dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
+          if (two) dev::mbar_wait(&bars[(c + 1) % stages], static_cast<uint32_t>((c + 1) / stages) & 1u);
+          phase_a(dtag, sb[0], t0s[0], dd);
+          if (two) phase_a(dtag, sb[1], t0s[1], dd + kChainGroups * kRowStride);
+          __syncthreads();
+          // phase B, lane = tile, both blocks per row-table read
+          const uint32_t l0 = sb[0] + lane * 4u, l1 = sb[1] + lane * 4u;
+          const uint32_t d0 = dd_s + lane * 4u, d1 = d0 + kChainGroups * kRowStride * 4u;
+          const uint32_t m0 = lane >= t0s[0] && lane < t1s[0] ? ~0u : 0u;
+          const uint32_t m1 = two && lane >= t0s[1] && lane < t1s[1] ? ~0u : 0u;
+          for (int j = 0; j < nact; j += 4) {
+            const uint4 ro = dev::lds_v4(erow_s + j * 4u);
+            const uint4 go = dev::lds_v4(egrp_s + j * 4u);
+            uint4 a, b;
+            a.x = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.x) & dev::lds_u32(d0 + go.x) & m0) != 0u);
+            b.x = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.x) & dev::lds_u32(d1 + go.x) & m1) != 0u);
+            a.y = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.y) & dev::lds_u32(d0 + go.y) & m0) != 0u);
+            b.y = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.y) & dev::lds_u32(d1 + go.y) & m1) != 0u);
+            a.z = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.z) & dev::lds_u32(d0 + go.z) & m0) != 0u);
+            b.z = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.z) & dev::lds_u32(d1 + go.z) & m1) != 0u);
+            a.w = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.w) & dev::lds_u32(d0 + go.w) & m0) != 0u);
+            b.w = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.w) & dev::lds_u32(d1 + go.w) & m1) != 0u);
+            if (lane == 0) {
+              *reinterpret_cast<uint4*>(&cs.nz[0][wbase + j]) = a;
+              *reinterpret_cast<uint4*>(&cs.nz[1][wbase + j]) = b;
+            }
+          }
+          __syncwarp();
+          // phase C, lane = episode: block c's chain ends, then block c+1's
+          if (active) {
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              uint32_t mine = cs.nz[b][tid];
+              const uint32_t ro4 = sb[b] + cs.erow[tid];
+              const uint32_t go4 = dd_s + b * kChainGroups * kRowStride * 4u + cs.egrp[tid];
+              const int32_t base_rel = gbs[b] - g0;
+              while (mine) {
+                const int t = __ffs(mine) - 1;
+                mine &= mine - 1u;
+                const uint32_t w = dev::lds_u32(ro4 + t * 4u) & dev::lds_u32(go4 + t * 4u);
+                if (bound)
+                  st.cnt += 32 * (base_rel + t) >= cx.tq ? __popc(w) : 0u;
+                else
+                  chain_word<N, W>(cx, st, w, 32 * (base_rel + t));
+              }
+            }
+          }
+          __syncthreads();  // stage slots and DD rows free for reuse
+        }
+        return;
+      }
+    }
     for (int32_t c = 0; c < nblk; ++c) {
       const int32_t gb = (blk0 + c) * 32;
       const int32_t t0 = g0 > gb ? g0 - gb : 0;
       const int32_t t1 = gend - gb < 32 ? gend - gb : 32;
-      if (tid == 0 && c + stages - 1 < nblk) issue(c + stages - 1);
+      if (tid == 0 && c + ahead < nblk) issue(c + ahead);
       dev::mbar_wait(&bars[c % stages], static_cast<uint32_t>(c / stages) & 1u);
       const uint32_t sbase_s = stage_s + static_cast<uint32_t>(c % stages) * bw * 4u;
       if constexpr (D > 0) {
-        phase_a(dtag, sbase_s, t0);
+        phase_a(dtag, sbase_s, t0, dd);
         __syncthreads();
       }
       const int32_t base_rel = gb - g0 * 1;  // tile offset of this block from g0
@@ -375,12 +451,12 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
           m.y = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.y) & dev::lds_u32(dlane_s + go.y) & msk) != 0u);
           m.z = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.z) & dev::lds_u32(dlane_s + go.z) & msk) != 0u);
           m.w = __ballot_sync(0xffffffffu, (dev::lds_u32(lane_s + ro.w) & dev::lds_u32(dlane_s + go.w) & msk) != 0u);
-          if (lane == 0) *reinterpret_cast<uint4*>(&cs.nz[wbase + j]) = m;
+          if (lane == 0) *reinterpret_cast<uint4*>(&cs.nz[0][wbase + j]) = m;
         }
         __syncwarp();
         // phase C: lane = episode, its chain-end tiles in time order
         if (active) {
-          uint32_t mine = cs.nz[tid];
+          uint32_t mine = cs.nz[0][tid];
           const uint32_t ro4 = sbase_s + cs.erow[tid];
           const uint32_t go4 = dd_s + cs.egrp[tid];
           while (mine) {

@@ -527,6 +527,11 @@ void Engine::count_device(const DevSet& ds, uint64_t* d_counts, epi_stats& stats
   const bool dedup = chain && n >= (std::getenv("EPI_CHAIN") ? 1 : 65536) && !std::getenv("EPI_NO_DEDUP") &&
                      !capturing_ && !tshard_;
   if (chain) {
+    // a 4-deep staging ring lets row-mode CTAs take two bitmap blocks per
+    // iteration (chain_impl.cuh) when the blocks are small enough; large sets
+    // are the ones whose CTAs share whole prefixes (row mode) - small ones
+    // keep the 3-deep ring and its occupancy
+    if (n >= 65536 && p.blk_words * 4u * 4u <= 48u * 1024u) p.stages = 4;
     char* sc = scratch_.get<char>(kSlotChainSort, chain_sort_scratch(n, N));
     const int own = chain_sort({ds.types, ds.win, ds.sigma, n, N, stream_.alphabet}, dedup, sc, so, st_);
     stats.kernel_launches += static_cast<uint64_t>(own);
