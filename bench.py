@@ -333,8 +333,12 @@ def run_ours(args, rank, world, local_rank):
         types, times = ctx.download()
         alphabet = alphabet_of(sp)
     else:
-        types, times, alphabet = make_stream(args.config, args.cfg5_events)
-        ctx.load_arrays(types, times, alphabet)
+        # cfg4's bursty MEA-shaped stream, also generated on the device
+        from paper_0905_2203_b200 import BurstConfig, Embedding, Episode
+        ctx.generate_bursty(BurstConfig(electrodes=sp["electrodes"], duration_s=sp["duration_s"], seed=sp["seed"],
+                                        embedded=[Embedding(Episode(t, c), r) for t, c, r in sp["embedded"]]))
+        types, times = ctx.download()
+        alphabet = alphabet_of(sp)
     n = len(types)
 
     # Pinned host copies for the end-to-end leg.

@@ -250,6 +250,14 @@ void epi_free(void* p);
  * stream takes a fraction of a second instead of host minutes. */
 epi_status epi_generate_stream(epi_ctx* ctx, uint32_t neurons, double duration_s, double base_rate_hz,
                                uint64_t seed, const epi_episode_batch* embedded, const double* rates);
+/* epi_generate_bursty's MEA-shaped stream (cfg4) generated on the device
+ * straight into the context, identical to the host generator's output: the
+ * per-electrode rates and the burst schedule are planned on the host, each
+ * electrode's background and burst events drawn by one CTA. */
+epi_status epi_generate_bursty_stream(epi_ctx* ctx, uint32_t electrodes, double duration_s,
+                                      double base_rate_hz, double rate_sigma, double burst_rate_hz,
+                                      double burst_min_ms, double burst_max_ms, double burst_gain,
+                                      uint64_t seed, const epi_episode_batch* embedded, const double* rates);
 /* Copies the loaded stream (epi_stream_size events) to host arrays. */
 epi_status epi_stream_download(epi_ctx* ctx, uint32_t* types_out, int64_t* times_out);
 

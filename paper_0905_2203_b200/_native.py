@@ -100,7 +100,7 @@ EXPORTS = ("epi_create", "epi_destroy", "epi_last_error", "epi_status_name", "ep
            "epi_mine_sharded", "epi_count_sharded", "epi_write_events", "epi_read_events",
            "epi_load_stream_file", "epi_random_episodes", "epi_count_mapconcat", "epi_create_multi",
            "epi_world", "epi_uses_nccl", "epi_stream_upload_bytes", "epi_generate_stream",
-           "epi_stream_download")
+           "epi_stream_download", "epi_generate_bursty_stream")
 
 
 def _load() -> C.CDLL:
@@ -147,6 +147,9 @@ def _load() -> C.CDLL:
         "epi_generate_stream": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_double, C.c_uint64,
                                           C.POINTER(EpisodeBatch), f64p]),
         "epi_stream_download": (C.c_int, [C.c_void_p, u32p, i64p]),
+        "epi_generate_bursty_stream": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                                 C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                                 C.POINTER(EpisodeBatch), f64p]),
         "epi_generate_bursty": (C.c_int, [C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_double,
                                           C.c_double, C.c_double, C.c_double, C.c_uint64,
                                           C.POINTER(EpisodeBatch), f64p, C.POINTER(u32p),

@@ -253,6 +253,20 @@ class Context:
                                               C.byref(csr.struct) if csr is not None else None,
                                               N.ptr(rates, C.c_double) if len(rates) else None))
 
+    def generate_bursty(self, cfg: "BurstConfig"):
+        """The MEA-shaped bursty stream (generate_bursty_arrays) generated on
+        the device and loaded as this context's stream
+        (epi_generate_bursty_stream)."""
+        eps = [e.episode for e in cfg.embedded]
+        csr = episodes_to_csr(eps) if eps else None
+        rates = np.array([e.rate_hz for e in cfg.embedded], dtype=np.float64)
+        self._loaded = None
+        self._check(N.lib.epi_generate_bursty_stream(
+            self._h, int(cfg.electrodes), float(cfg.duration_s), float(cfg.base_rate_hz), float(cfg.rate_sigma),
+            float(cfg.burst_rate_hz), float(cfg.burst_min_ms), float(cfg.burst_max_ms), float(cfg.burst_gain),
+            int(cfg.seed) & ((1 << 64) - 1), C.byref(csr.struct) if csr is not None else None,
+            N.ptr(rates, C.c_double) if len(rates) else None))
+
     def download(self):
         """(types, times) of the loaded stream (epi_stream_download)."""
         n = int(N.lib.epi_stream_size(self._h))

@@ -358,6 +358,24 @@ epi_status epi_generate_stream(epi_ctx* ctx, uint32_t neurons, double duration_s
   });
 }
 
+epi_status epi_generate_bursty_stream(epi_ctx* ctx, uint32_t electrodes, double duration_s,
+                                      double base_rate_hz, double rate_sigma, double burst_rate_hz,
+                                      double burst_min_ms, double burst_max_ms, double burst_gain,
+                                      uint64_t seed, const epi_episode_batch* embedded, const double* rates) {
+  if (!ctx) return EPI_EINVAL;
+  std::lock_guard<std::mutex> lk(ctx->engine.mu);
+  return guarded(ctx->engine.err, [&] {
+    auto one = [&](epi::Engine& e) {
+      e.generate_bursty_device(electrodes, duration_s, base_rate_hz, rate_sigma, burst_rate_hz, burst_min_ms,
+                               burst_max_ms, burst_gain, seed, embedded, rates);
+    };
+    if (ctx->multi)
+      ctx->multi->run([&](int r, const epi_shard&) { one(ctx->multi->rank(r)); }, 0);
+    else
+      one(ctx->engine);
+  });
+}
+
 epi_status epi_stream_download(epi_ctx* ctx, uint32_t* types_out, int64_t* times_out) {
   if (!ctx) return EPI_EINVAL;
   std::lock_guard<std::mutex> lk(ctx->engine.mu);

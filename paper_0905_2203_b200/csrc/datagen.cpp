@@ -198,6 +198,39 @@ void generate_embedded_events(uint32_t neurons, double duration_s, uint64_t seed
   }
 }
 
+// The host-side parts of generate_bursty for the device generator
+// (gen_dev.cu): the per-electrode rates (the first two draws of each
+// electrode's Rng, Box-Muller, exp - computed here so that libm decides them
+// exactly as in generate_bursty) and the shared burst schedule.
+void bursty_plan(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                 double burst_rate_hz, double burst_min_ms, double burst_max_ms, double burst_gain, uint64_t seed,
+                 std::vector<double>& rates, std::vector<double>& burst_lo, std::vector<double>& burst_hi) {
+  if (electrodes < 1) throw Error(EPI_EINVAL, "generate: need at least one neuron");
+  if (duration_s < 0) throw Error(EPI_EINVAL, "generate: negative duration");
+  if (!(base_rate_hz > 0)) throw Error(EPI_EINVAL, "generate: base rate must be > 0");
+  if (!(burst_gain >= 1) || burst_rate_hz < 0 || burst_min_ms < 0 || burst_max_ms < burst_min_ms)
+    throw Error(EPI_EINVAL, "generate_bursty: invalid burst parameters");
+  burst_lo.clear();
+  burst_hi.clear();
+  if (burst_rate_hz > 0) {
+    Rng rb(splitmix64(seed ^ 0xB1257ULL));
+    double t = rb.exponential(burst_rate_hz);
+    while (t < duration_s) {
+      const double len = (burst_min_ms + (burst_max_ms - burst_min_ms) * rb.uniform01()) / 1000.0;
+      burst_lo.push_back(t);
+      burst_hi.push_back(std::min(t + len, duration_s));
+      t += len + rb.exponential(burst_rate_hz);
+    }
+  }
+  rates.resize(electrodes);
+  for (uint32_t e = 0; e < electrodes; ++e) {
+    Rng rng(splitmix64(seed ^ (0xB0B5ULL + e)));
+    const double u1 = rng.uniform01(), u2 = rng.uniform01();
+    const double z = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+    rates[e] = base_rate_hz * std::exp(rate_sigma * z);
+  }
+}
+
 // MEA-culture-shaped bursty generator (the reference
 // generator has no burst model, E/datagen.hpp:91-98). Deterministic under a
 // seed, with the reference's Rng (mt19937_64 raw output + splitmix64 seeds):

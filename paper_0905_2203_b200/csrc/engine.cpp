@@ -37,7 +37,7 @@ enum Slot : size_t {
   // tracking counter (tracking.cu)
   kSlotChainSort = 60,
   kSlotChainCounts = 61,
-  // 62: the device generator's keys and sort buffers (gen_dev.cu)
+  // 62, 63: the device generators' keys, sort buffers and plans (gen_dev.cu)
 };
 
 constexpr uint64_t kPruned = EPI_COUNT_PRUNED;

@@ -96,6 +96,11 @@ class Engine {
   // context's stream (gen_dev.cu).
   void generate_stream_device(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
                               const epi_episode_batch* emb, const double* rates);
+  // generate_bursty (datagen.cpp, cfg4's MEA-shaped stream) bit-exact on the
+  // device (gen_dev.cu; rates and the burst schedule are planned on the host).
+  void generate_bursty_device(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                              double burst_rate_hz, double burst_min_ms, double burst_max_ms, double burst_gain,
+                              uint64_t seed, const epi_episode_batch* emb, const double* rates);
   // Copies the loaded stream's SoA back to host arrays (stream_size entries).
   void download_stream(uint32_t* types, int64_t* times);
   void load_stream_device(const uint32_t* d_types, const int64_t* d_times, uint64_t n,

@@ -27,6 +27,9 @@ namespace epi {
 
 void generate_embedded_events(uint32_t neurons, double duration_s, uint64_t seed, const epi_episode_batch* emb,
                               const double* rates, std::vector<uint32_t>& types, std::vector<int64_t>& times);
+void bursty_plan(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                 double burst_rate_hz, double burst_min_ms, double burst_max_ms, double burst_gain, uint64_t seed,
+                 std::vector<double>& rates, std::vector<double>& burst_lo, std::vector<double>& burst_hi);
 
 namespace {
 
@@ -115,6 +118,96 @@ __global__ void __launch_bounds__(kGenThreads)
   }
 }
 
+// generate_bursty (datagen.cpp) per electrode: the first
+// two draws went into the electrode's rate (computed on the host), then the
+// background Poisson process at rate r until the duration, then, burst after
+// burst, extra events at r * (gain - 1) inside each burst window - one draw
+// stream, consumed in exactly that order.
+__global__ void __launch_bounds__(kGenThreads)
+    bursty_kernel(uint64_t seed, double duration_s, const double* __restrict__ rates, double gain,
+                  const double* __restrict__ blo, const double* __restrict__ bhi, uint32_t nb, uint32_t tb, uint64_t cap,
+                  uint64_t* keys, unsigned long long* counts, unsigned int* overflow) {
+  __shared__ uint64_t mt[kMtN];
+  __shared__ double gbg[kMtN], gbu[kMtN];
+  __shared__ int done;
+  const uint32_t el = blockIdx.x;
+  const int tid = threadIdx.x;
+  const double r = rates[el];
+  const double extra = r * (gain - 1.0);
+  if (tid == 0) {
+    mt[0] = splitmix64_d(seed ^ (0xB0B5ull + el));
+    for (int i = 1; i < kMtN; ++i) mt[i] = 6364136223846793005ull * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+    done = 0;
+  }
+  __syncthreads();
+  uint64_t* out = keys + static_cast<uint64_t>(el) * cap;
+  // sequential state (thread 0): phase 0 background, 1 bursts, 2 done
+  int phase = 0, skip = 2;
+  bool first = true, bstart = true;
+  double t = 0.0, s_t = 0.0;
+  uint32_t bi = 0;
+  uint64_t cnt = 0;
+  auto push = [&](double x) {
+    const uint64_t ms = static_cast<uint64_t>(static_cast<int64_t>(x * 1000.0));
+    if (cnt < cap) out[cnt] = (ms << tb) | el;
+    ++cnt;
+  };
+  for (;;) {
+    uint64_t nv = 0;
+    if (tid < kMtN - kMtM) {
+      const uint64_t x = (mt[tid] & kUpper) | (mt[tid + 1] & kLower);
+      nv = mt[tid + kMtM] ^ (x >> 1) ^ ((x & 1ull) ? kMatrixA : 0ull);
+    }
+    __syncthreads();
+    if (tid < kMtN - kMtM) mt[tid] = nv;
+    __syncthreads();
+    if (tid >= kMtN - kMtM && tid < kMtN) {
+      const uint64_t x = (mt[tid] & kUpper) | (mt[(tid + 1) % kMtN] & kLower);
+      nv = mt[tid - (kMtN - kMtM)] ^ (x >> 1) ^ ((x & 1ull) ? kMatrixA : 0ull);
+    }
+    __syncthreads();
+    if (tid >= kMtN - kMtM && tid < kMtN) mt[tid] = nv;
+    __syncthreads();
+    if (tid < kMtN) {
+      const double u = (static_cast<double>(temper(mt[tid]) >> 11) + 1.0) * 0x1.0p-53;
+      const double lg = -log(u);
+      gbg[tid] = lg / r;                           // exponential(r)
+      gbu[tid] = extra > 0 ? lg / extra : 0.0;     // exponential(extra)
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = skip; i < kMtN && phase < 2; ++i) {
+        if (phase == 0) {
+          t = first ? gbg[i] : t + gbg[i];
+          first = false;
+          if (!(t < duration_s)) {
+            phase = extra > 0 && nb > 0 ? 1 : 2;
+            continue;
+          }
+          push(t);
+        } else {
+          s_t = bstart ? blo[bi] + gbu[i] : s_t + gbu[i];
+          bstart = false;
+          if (!(s_t < bhi[bi])) {
+            bstart = true;
+            if (++bi == nb) phase = 2;
+            continue;
+          }
+          push(s_t);
+        }
+      }
+      skip = 0;
+      if (phase == 2) done = 1;
+    }
+    __syncthreads();
+    if (done) break;
+  }
+  if (tid == 0) {
+    counts[el] = cnt;
+    if (cnt > cap) atomicOr(overflow, 1u);
+  }
+}
+
 __global__ void decode_keys_kernel(const uint64_t* __restrict__ keys, uint64_t n, uint32_t tb, uint32_t* types,
                                    int64_t* times) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -126,9 +219,77 @@ __global__ void decode_keys_kernel(const uint64_t* __restrict__ keys, uint64_t n
 
 inline size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
-constexpr size_t kSlotGen = 62;  // engine scratch slot (see engine.cpp's slot map)
+constexpr size_t kSlotGen = 62;      // engine scratch slots (see engine.cpp's slot map)
+constexpr size_t kSlotGenPlan = 63;
 
 }  // namespace
+
+// Key layout, sort and load shared by both device generators: `launch`
+// fills keys [0, units * cap) (per-unit event counts into counts[], an
+// overflow flag into *ovf) on the engine stream; the embedded events join at
+// the end; one radix sort over the key bits orders (time, type).
+template <class Launch>
+void gen_finish(Engine& eng, DeviceScratch& scratch, DeviceStream& stream, cudaStream_t st, uint32_t units,
+                uint32_t alphabet, uint64_t cap, int64_t max_ms, const std::vector<uint32_t>& et,
+                const std::vector<int64_t>& etm, uint64_t& h2d, Launch&& launch) {
+  uint32_t tb = 1;
+  while ((1ull << tb) < alphabet) ++tb;
+  for (int64_t x : etm) max_ms = std::max(max_ms, x);
+  uint32_t time_bits = 1;
+  while ((1ull << time_bits) <= static_cast<uint64_t>(max_ms) + 1) ++time_bits;
+  const uint32_t key_bits = time_bits + tb;
+  if (key_bits > 64) throw Error(EPI_EUNSUPPORTED, "generate: stream span too long for the device generator");
+  const uint64_t ne = et.size();
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t slots = static_cast<uint64_t>(units) * cap + ne;
+    if (slots >= (1ull << 31)) throw Error(EPI_EUNSUPPORTED, "generate: more than 2^31 event slots on the device");
+    size_t temp_bytes = 0;
+    EPI_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, static_cast<const uint64_t*>(nullptr),
+                                            static_cast<uint64_t*>(nullptr), static_cast<int>(slots), 0,
+                                            static_cast<int>(key_bits)));
+    const size_t o_a = 0, o_b = align256(slots * 8), o_cnt = o_b + align256(slots * 8),
+                 o_tmp = o_cnt + align256((units + 1) * 8ull), total = o_tmp + align256(temp_bytes);
+    char* d = scratch.get<char>(kSlotGen, total);
+    uint64_t* ka = reinterpret_cast<uint64_t*>(d + o_a);
+    uint64_t* kb = reinterpret_cast<uint64_t*>(d + o_b);
+    unsigned long long* counts = reinterpret_cast<unsigned long long*>(d + o_cnt);
+    unsigned int* ovf = reinterpret_cast<unsigned int*>(counts + units);
+    // all-ones keys sort after every event key over the key bits
+    EPI_CUDA(cudaMemsetAsync(ka, 0xff, slots * 8, st));
+    EPI_CUDA(cudaMemsetAsync(ovf, 0, 4, st));
+    launch(tb, cap, ka, counts, ovf);
+    EPI_CUDA(cudaGetLastError());
+    if (ne) {
+      std::vector<uint64_t> ek(ne);
+      for (uint64_t i = 0; i < ne; ++i) ek[i] = (static_cast<uint64_t>(etm[i]) << tb) | et[i];
+      EPI_CUDA(cudaMemcpyAsync(ka + static_cast<uint64_t>(units) * cap, ek.data(), ne * 8, cudaMemcpyHostToDevice, st));
+    }
+    std::vector<unsigned long long> hc(units + 1);
+    EPI_CUDA(cudaMemcpyAsync(hc.data(), counts, (units + 1) * 8ull, cudaMemcpyDeviceToHost, st));
+    EPI_CUDA(cudaStreamSynchronize(st));
+    if (reinterpret_cast<const unsigned int*>(&hc[units])[0] != 0) {
+      if (attempt >= 3) throw Error(EPI_EUNSUPPORTED, "generate: per-unit event capacity exceeded");
+      cap *= 2;
+      continue;
+    }
+    uint64_t n = ne;
+    for (uint32_t i = 0; i < units; ++i) n += hc[i];
+    cub::DoubleBuffer<uint64_t> db(ka, kb);
+    size_t tb_bytes = temp_bytes;
+    EPI_CUDA(cub::DeviceRadixSort::SortKeys(d + o_tmp, tb_bytes, db, static_cast<int>(slots), 0,
+                                            static_cast<int>(key_bits), st));
+    stream.reserve_raw(n);
+    if (n)
+      decode_keys_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(db.Current(), n, tb,
+                                                                                  stream.d_types_raw,
+                                                                                  stream.d_times_raw);
+    EPI_CUDA(cudaGetLastError());
+    h2d = ne * 8;
+    stream.load(n, alphabet, st, scratch);
+    (void)eng;
+    return;
+  }
+}
 
 void Engine::generate_stream_device(uint32_t neurons, double duration_s, double base_rate_hz, uint64_t seed,
                                     const epi_episode_batch* emb, const double* rates) {
@@ -139,66 +300,50 @@ void Engine::generate_stream_device(uint32_t neurons, double duration_s, double 
   std::vector<uint32_t> et;
   std::vector<int64_t> etm;
   generate_embedded_events(neurons, duration_s, seed, emb, rates, et, etm);
-  uint32_t tb = 1;
-  while ((1ull << tb) < neurons) ++tb;
-  // key = time_ms << tb | type; the sentinel (every key bit set) sorts last
-  int64_t max_ms = static_cast<int64_t>(duration_s * 1000.0) + 1;
-  for (int64_t x : etm) max_ms = std::max(max_ms, x);
-  uint32_t time_bits = 1;
-  while ((1ull << time_bits) <= static_cast<uint64_t>(max_ms) + 1) ++time_bits;
-  const uint32_t key_bits = time_bits + tb;
-  if (key_bits > 64) throw Error(EPI_EUNSUPPORTED, "generate: stream span too long for the device generator");
-  // per-neuron capacity: mean + 10 sigma (+ slack)
-  const double lambda = base_rate_hz * duration_s;
-  uint64_t cap = static_cast<uint64_t>(lambda + 10.0 * std::sqrt(lambda) + 1024.0);
-  const uint64_t ne = et.size();
-  for (int attempt = 0;; ++attempt) {
-    const uint64_t slots = static_cast<uint64_t>(neurons) * cap + ne;
-    size_t temp_bytes = 0;
-    EPI_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, temp_bytes, static_cast<const uint64_t*>(nullptr),
-                                            static_cast<uint64_t*>(nullptr), slots, 0, static_cast<int>(key_bits)));
-    const size_t o_a = 0, o_b = align256(slots * 8), o_cnt = o_b + align256(slots * 8),
-                 o_tmp = o_cnt + align256((neurons + 1) * 8ull), total = o_tmp + align256(temp_bytes);
-    char* d = scratch_.get<char>(kSlotGen, total);
-    uint64_t* ka = reinterpret_cast<uint64_t*>(d + o_a);
-    uint64_t* kb = reinterpret_cast<uint64_t*>(d + o_b);
-    unsigned long long* counts = reinterpret_cast<unsigned long long*>(d + o_cnt);
-    unsigned int* ovf = reinterpret_cast<unsigned int*>(counts + neurons);
-    // sentinel fill (a byte pattern: all-ones keys, trimmed to the key bits
-    // by the sort's bit range)
-    EPI_CUDA(cudaMemsetAsync(ka, 0xff, slots * 8, st_));
-    EPI_CUDA(cudaMemsetAsync(ovf, 0, 4, st_));
-    poisson_kernel<<<neurons, kGenThreads, 0, st_>>>(seed, duration_s, base_rate_hz, tb, cap, ka, counts, ovf);
-    EPI_CUDA(cudaGetLastError());
-    if (ne) {
-      std::vector<uint64_t> ek(ne);
-      for (uint64_t i = 0; i < ne; ++i) ek[i] = (static_cast<uint64_t>(etm[i]) << tb) | et[i];
-      EPI_CUDA(cudaMemcpyAsync(ka + static_cast<uint64_t>(neurons) * cap, ek.data(), ne * 8, cudaMemcpyHostToDevice,
-                               st_));
-    }
-    std::vector<unsigned long long> hc(neurons + 1);
-    EPI_CUDA(cudaMemcpyAsync(hc.data(), counts, (neurons + 1) * 8ull, cudaMemcpyDeviceToHost, st_));
-    EPI_CUDA(cudaStreamSynchronize(st_));
-    if (reinterpret_cast<const unsigned int*>(&hc[neurons])[0] != 0) {
-      if (attempt >= 2) throw Error(EPI_EUNSUPPORTED, "generate: per-neuron event capacity exceeded");
-      cap *= 2;
-      continue;
-    }
-    uint64_t n = ne;
-    for (uint32_t i = 0; i < neurons; ++i) n += hc[i];
-    cub::DoubleBuffer<uint64_t> db(ka, kb);
-    size_t tb_bytes = temp_bytes;
-    EPI_CUDA(cub::DeviceRadixSort::SortKeys(d + o_tmp, tb_bytes, db, slots, 0, static_cast<int>(key_bits), st_));
-    csr_valid_ = false;
-    stream_.reserve_raw(n);
-    if (n)
-      decode_keys_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st_>>>(
-          db.Current(), n, tb, stream_.d_types_raw, stream_.d_times_raw);
-    EPI_CUDA(cudaGetLastError());
-    last_load_h2d = ne * 8;
-    stream_.load(n, neurons, st_, scratch_);
-    return;
-  }
+  const double lambda = base_rate_hz * duration_s;  // per neuron: mean + 10 sigma
+  const uint64_t cap = static_cast<uint64_t>(lambda + 10.0 * std::sqrt(lambda) + 1024.0);
+  csr_valid_ = false;
+  gen_finish(*this, scratch_, stream_, st_, neurons, neurons, cap, static_cast<int64_t>(duration_s * 1000.0) + 1,
+             et, etm, last_load_h2d,
+             [&](uint32_t tb, uint64_t c, uint64_t* keys, unsigned long long* counts, unsigned int* ovf) {
+               poisson_kernel<<<neurons, kGenThreads, 0, st_>>>(seed, duration_s, base_rate_hz, tb, c, keys, counts,
+                                                                ovf);
+             });
+}
+
+void Engine::generate_bursty_device(uint32_t electrodes, double duration_s, double base_rate_hz, double rate_sigma,
+                                    double burst_rate_hz, double burst_min_ms, double burst_max_ms, double burst_gain,
+                                    uint64_t seed, const epi_episode_batch* emb, const double* rates) {
+  std::vector<double> er, blo, bhi;
+  bursty_plan(electrodes, duration_s, base_rate_hz, rate_sigma, burst_rate_hz, burst_min_ms, burst_max_ms,
+              burst_gain, seed, er, blo, bhi);
+  std::vector<uint32_t> et;
+  std::vector<int64_t> etm;
+  generate_embedded_events(electrodes, duration_s, seed, emb, rates, et, etm);
+  // capacity: the busiest electrode's background + burst events, + 10 sigma
+  double burst_s = 0;
+  for (size_t b = 0; b < blo.size(); ++b) burst_s += bhi[b] - blo[b];
+  double rmax = 0;
+  for (double r : er) rmax = std::max(rmax, r);
+  const double lambda = rmax * duration_s + rmax * (burst_gain - 1.0) * burst_s;
+  const uint64_t cap = static_cast<uint64_t>(lambda + 10.0 * std::sqrt(lambda) + 1024.0);
+  // plan arrays on the device (rates, burst windows)
+  const size_t nb = blo.size();
+  std::vector<double> plan(electrodes + 2 * nb);
+  std::copy(er.begin(), er.end(), plan.begin());
+  std::copy(blo.begin(), blo.end(), plan.begin() + electrodes);
+  std::copy(bhi.begin(), bhi.end(), plan.begin() + electrodes + nb);
+  double* d_plan = scratch_.get<double>(kSlotGenPlan, plan.size() + 1);
+  EPI_CUDA(cudaMemcpyAsync(d_plan, plan.data(), plan.size() * 8, cudaMemcpyHostToDevice, st_));
+  csr_valid_ = false;
+  gen_finish(*this, scratch_, stream_, st_, electrodes, electrodes, cap,
+             static_cast<int64_t>(duration_s * 1000.0) + 1, et, etm, last_load_h2d,
+             [&](uint32_t tb, uint64_t c, uint64_t* keys, unsigned long long* counts, unsigned int* ovf) {
+               bursty_kernel<<<electrodes, kGenThreads, 0, st_>>>(seed, duration_s, d_plan, burst_gain,
+                                                                  d_plan + electrodes, d_plan + electrodes + nb,
+                                                                  static_cast<uint32_t>(nb), tb, c, keys, counts, ovf);
+             });
+  last_load_h2d += plan.size() * 8;
 }
 
 }  // namespace epi

@@ -84,3 +84,36 @@ def test_device_generate_errors(ctx):
         ctx.generate(GenConfig(4, 10, 0, [], 1))
     with pytest.raises(InvalidArgument, match="unknown neuron"):
         ctx.generate(GenConfig(4, 10, 20, [Embedding(Episode([0, 9], [(0, 5)]), 1.0)], 1))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(electrodes=12, duration_s=300, seed=7),
+    dict(electrodes=5, duration_s=50, seed=9, burst_gain=1.0),
+    dict(electrodes=7, duration_s=80, seed=11, burst_rate_hz=0.0),
+    dict(electrodes=9, duration_s=120, seed=13, burst_rate_hz=2.0, burst_min_ms=5, burst_max_ms=40),
+])
+def test_device_bursty_equals_host(ctx, cfg):
+    """epi_generate_bursty_stream == the host bursty generator (element-wise),
+    with and without bursts, extra rate 0, short dense bursts, embedded
+    episodes."""
+    from paper_0905_2203_b200 import BurstConfig, generate_bursty_arrays
+    bc = BurstConfig(embedded=[Embedding(Episode([0, 1, 2], [(5, 10), (0, 5)]), 0.7)], **cfg)
+    ht, htm = generate_bursty_arrays(bc)
+    ctx.generate_bursty(bc)
+    types, times = ctx.download()
+    np.testing.assert_array_equal(types, ht)
+    np.testing.assert_array_equal(times, htm)
+
+
+def test_device_bursty_cfg4_matches_fixture(ctx):
+    """cfg4's ~100M-event stream generated on the device: the digest the
+    reference-checked scale fixture was computed on."""
+    from paper_0905_2203_b200 import BurstConfig
+    cell = json.load(open(os.path.join(GOLDEN, "scale.json")))["cfg4"]
+    s = cell["stream"]
+    emb = [Embedding(Episode(t, [tuple(c) for c in cs]), s["embedded_rate_hz"]) for t, cs in cell["extra"]]
+    ctx.generate_bursty(BurstConfig(electrodes=s["electrodes"], duration_s=s["duration_s"], seed=s["seed"],
+                                    embedded=emb))
+    types, times = ctx.download()
+    assert len(types) == cell["n"]
+    assert oracle.fnv_stream(types, times, cell["alphabet"]) == cell["stream_fnv"]

@@ -49,8 +49,12 @@ def stream_of(cell, ctx=None):
         types, times = generate_arrays(GenConfig(s["neurons"], s["duration_s"], s["rate_hz"], [], s["seed"]))
     else:
         emb = [Embedding(Episode(t, [tuple(c) for c in cs]), s["embedded_rate_hz"]) for t, cs in cell["extra"]]
-        types, times = generate_bursty_arrays(BurstConfig(electrodes=s["electrodes"], duration_s=s["duration_s"],
-                                                          seed=s["seed"], embedded=emb))
+        bc = BurstConfig(electrodes=s["electrodes"], duration_s=s["duration_s"], seed=s["seed"], embedded=emb)
+        if ctx is not None:
+            ctx.generate_bursty(bc)
+            types, times = ctx.download()
+        else:
+            types, times = generate_bursty_arrays(bc)
     assert len(types) == cell["n"]
     assert oracle.fnv_stream(types, times, cell["alphabet"]) == cell["stream_fnv"]
     return types, times
@@ -103,8 +107,7 @@ def test_cfg3_all_candidates(ctx, scale, kernel, monkeypatch):
     if kernel == "automaton":
         monkeypatch.setenv("EPI_CHAIN", "0")
     cell = scale["cfg3"]
-    types, times = stream_of(cell)
-    ctx.load_arrays(types, times, cell["alphabet"])
+    types, times = stream_of(cell, ctx)
     got = ctx.count_csr(cands_of(cell))
     want = np.array(cell["counts"], np.uint64)
     bad = np.nonzero(got != want)[0]
@@ -116,8 +119,7 @@ def test_cfg4_mea_bursty_100m(ctx, scale):
     """cfg4: the first 1,000 seeded 5-node candidates + the embedded chains
     over ~100M bursty events == the reference; properties on all of them."""
     cell = scale["cfg4"]
-    types, times = stream_of(cell)
-    ctx.load_arrays(types, times, cell["alphabet"])
+    types, times = stream_of(cell, ctx)
     csr = cands_of(cell)
     got = ctx.count_csr(csr)
     np.testing.assert_array_equal(got, np.array(cell["counts"], np.uint64))
