@@ -542,7 +542,11 @@ def run_ours(args, rank, world, local_rank):
         "pass_breakdown": {k: stats[-1][k] for k in ("episodes", "pass1_groups", "pass2_episodes",
                                                       "pruned", "segments", "patches", "pass1_ms",
                                                       "pass2_ms", "map_ms", "concat_ms", "bound_ms",
-                                                      "total_ms")},
+                                                      "total_ms", "chain_launches")},
+        # the work counted exactly (pass 2) as its own rate next to `value`
+        # (which counts every candidate, pruned or not): on the exact-count
+        # configs the two are equal; on cfg2 the difference is pass-1 pruning
+        "exact_episode_events_per_s": sum(s["pass2_episodes"] for s in stats) * n / (step_ms * 1e-3),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_for(args, types, times, alphabet)
