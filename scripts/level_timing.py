@@ -2,8 +2,8 @@
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
-from paper_0905_2203_b200 import Context, MODE_MINE, generate_arrays
-types, times = generate_arrays(bench.make_config("cfg2"))
+from paper_0905_2203_b200 import Context, MODE_MINE
+types, times, _ = bench.make_stream("cfg2")
 ctx = Context(0)
 ctx.load_arrays(types, times, 26)
 for it in range(5):

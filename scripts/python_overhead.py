@@ -2,8 +2,8 @@ import os, sys, time, ctypes as C
 sys.path.insert(0, "/root/repo")
 import numpy as np
 import bench
-from paper_0905_2203_b200 import Context, MODE_MINE, generate_arrays, _native as N
-types, times = generate_arrays(bench.make_config("cfg2"))
+from paper_0905_2203_b200 import Context, MODE_MINE, _native as N
+types, times, _ = bench.make_stream("cfg2")
 ctx = Context(0)
 ctx.load_arrays(types, times, 26)
 for _ in range(5): ctx.mine_raw(250, bench.BINS, 4, MODE_MINE)

@@ -2,13 +2,12 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
-from paper_0905_2203_b200 import Context, generate_arrays
+from paper_0905_2203_b200 import Context
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
-types, times = generate_arrays(bench.make_config(cfg))
+types, times, a = bench.make_stream(cfg)
 ctx = Context(0)
-ctx.load_arrays(types, times, 64 if cfg == "cfg3" else 26)
-eps = bench.cfg3_candidates() if cfg == "cfg3" else bench.cfg1_candidates()
-csr = bench.to_csr(eps)
+ctx.load_arrays(types, times, a)
+csr = bench.count_candidates_csr(cfg)
 for P in [None] + [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "8,11,15,18,22,26,29,37,44,59,74,89,118").split(",")]:
     if P is None:
         os.environ.pop("EPI_FORCE_SEGMENTS", None)

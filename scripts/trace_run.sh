@@ -3,8 +3,8 @@ python scripts/python_overhead.py > gpurun_out/trace.txt 2>&1
 EPI_TRACE=1 python - >> gpurun_out/trace.txt 2>&1 <<'PY'
 import sys; sys.path.insert(0,'.')
 import bench
-from paper_0905_2203_b200 import Context, MODE_MINE, generate_arrays
-types, times = generate_arrays(bench.make_config("cfg2"))
+from paper_0905_2203_b200 import Context, MODE_MINE
+types, times, _ = bench.make_stream("cfg2")
 ctx = Context(0); ctx.load_arrays(types, times, 26)
 for i in range(8):
     print("---- iter", i, file=sys.stderr, flush=True)

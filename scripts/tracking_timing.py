@@ -7,7 +7,8 @@ import bench
 from paper_0905_2203_b200 import Context
 for cfg, k in (("cfg1", None), ("cfg3", 1000)):
     types, times, a = bench.make_stream(cfg)
-    eps = bench.count_candidates(cfg)[:k] if k else bench.count_candidates(cfg)
+    full = bench.count_candidates_csr(cfg)
+    eps = [full.episode(i) for i in range(k or len(full))]
     csr = bench.to_csr(eps)
     ctx = Context(0)
     ctx.load_arrays(types, times, a)
