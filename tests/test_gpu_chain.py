@@ -160,3 +160,33 @@ def test_mine_mode_popcount_pass1(ctx, kind):
     st = ctx.last_stats
     assert st["pass1_groups"] == len(eps) and st["pruned"] == int((~keep).sum())
     assert st["chain_launches"] >= 1
+
+
+@pytest.mark.parametrize("alphabet", [120, 300])
+def test_chain_large_alphabet_two_stage_ring(ctx, chain_env, alphabet):
+    """Alphabets whose bitmap blocks no longer fit three (or four) staging
+    buffers: the chain kernel runs with the 2-deep ring."""
+    rng = np.random.default_rng(alphabet)
+    types, times = _stream(rng, 200_000, alphabet, "sparse")
+    ctx.load_arrays(types, times, alphabet)
+    eps = _uniform_batch(rng, alphabet, 5000, 5, 3, 200)
+    want = port_counts(types, times, eps)
+    for depth in (None, 1, 3):
+        chain_env(depth)
+        np.testing.assert_array_equal(ctx.count_csr(csr_of(eps)), want)
+
+
+@pytest.mark.parametrize("n_nodes", [6, 7, 8])
+def test_chain_long_episodes_large_sets(ctx, n_nodes, monkeypatch):
+    """Long episodes in sets large enough for the default chain path, the
+    dedup and the 4-deep ring (>= 65,536 episodes), against the port on a
+    subset and against the automaton kernel on all of them."""
+    rng = np.random.default_rng(n_nodes)
+    types, times = _stream(rng, 100_000, 6, "dense")
+    ctx.load_arrays(types, times, 6)
+    eps = _uniform_batch(rng, 6, 70_000, 3, n_nodes, 400)
+    got = ctx.count_csr(csr_of(eps))
+    assert ctx.last_stats["chain_launches"] >= 1
+    np.testing.assert_array_equal(got[:300], port_counts(types, times, eps[:300]))
+    monkeypatch.setenv("EPI_CHAIN", "0")
+    np.testing.assert_array_equal(got, ctx.count_csr(csr_of(eps)))
