@@ -141,3 +141,32 @@ def test_generate_candidates_empty_and_level1():
     assert generate_candidates(2, [], [(5, 10)], 3) == []
     assert generate_candidates(5, [], [(5, 10)], 3) == []
     assert generate_candidates(1, [], [(5, 10)], 2) == [Episode([0], []), Episode([1], [])]
+
+
+def test_reference_arm_loads_only_the_reference():
+    """bench.py --impl reference runs the reference compiled in place
+    (oracle/_ref) and nothing of this package: its JSON line lists the
+    in-repo shared objects the process loaded."""
+    import json
+    import subprocess
+    import sys
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0
+    libs = line["native_so_loaded"]
+    assert any("oracle/_ref" in p for p in libs), libs
+    assert not any("paper_0905_2203_b200" in p for p in libs), libs
+
+
+def test_reference_arm_candidates_equal_product_draws():
+    """The reference arm's pure-Python candidate draws (oracle.mt_episodes)
+    == this package's seeded generator (epi_random_episodes, host code)."""
+    from paper_0905_2203_b200 import random_episodes_csr
+    for seed, nodes, alphabet in ((55, 3, 64), (44, 5, 60), (5, 3, 64)):
+        eps = oracle.mt_episodes(seed, 200, nodes, alphabet, [(0, 5), (5, 10), (10, 15)])
+        csr = random_episodes_csr(seed, 200, nodes, alphabet, [(0, 5), (5, 10), (10, 15)])
+        assert [csr.episode(i) for i in range(200)] == [(list(t), [tuple(c) for c in cs]) for t, cs in eps]
