@@ -260,10 +260,15 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
       cs.carry[grp][k] = 0;
     }
   }
+  // row mode: the warp's episodes fall into runs of one group (sorted): the
+  // run heads (segmask) let phase B load each run's DD word once
+  const uint32_t my_go = static_cast<uint32_t>(grp > 0 ? grp : 0) * kRowStride * 4u;
+  const uint32_t my_ro = ep.type[N - 1] * kRowStride * 4u;
+  const uint32_t segmask =
+      __ballot_sync(0xffffffffu, active && (lane == 0 || __shfl_up_sync(0xffffffffu, my_go, 1) != my_go));
   if (dsel == M) {
-    const uint32_t eg = static_cast<uint32_t>(grp > 0 ? grp : 0) * kRowStride * 4u;
-    cs.erow[tid] = ep.type[N - 1] * kRowStride * 4u;
-    cs.egrp[tid] = eg;
+    cs.erow[tid] = my_ro;
+    cs.egrp[tid] = my_go;
   }
 
   // ---- per-segment greedy state ---------------------------------------------
@@ -353,7 +358,6 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
 
     if constexpr (D == M) {
       if (pair) {
-        const uint32_t erow_s = dev::smem_addr(&cs.erow[wbase]), egrp_s = dev::smem_addr(&cs.egrp[wbase]);
         for (int32_t c = 0; c < nblk; c += 2) {
           const bool two = c + 1 < nblk;
           if (tid == 0) {
@@ -380,21 +384,40 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
           const uint32_t d0 = dd_s + lane * 4u, d1 = d0 + kChainGroups * kRowStride * 4u;
           const uint32_t m0 = lane >= t0s[0] && lane < t1s[0] ? ~0u : 0u;
           const uint32_t m1 = two && lane >= t0s[1] && lane < t1s[1] ? ~0u : 0u;
-          for (int j = 0; j < nact; j += 4) {
-            const uint4 ro = dev::lds_v4(erow_s + j * 4u);
-            const uint4 go = dev::lds_v4(egrp_s + j * 4u);
-            uint4 a, b;
-            a.x = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.x) & dev::lds_u32(d0 + go.x) & m0) != 0u);
-            b.x = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.x) & dev::lds_u32(d1 + go.x) & m1) != 0u);
-            a.y = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.y) & dev::lds_u32(d0 + go.y) & m0) != 0u);
-            b.y = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.y) & dev::lds_u32(d1 + go.y) & m1) != 0u);
-            a.z = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.z) & dev::lds_u32(d0 + go.z) & m0) != 0u);
-            b.z = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.z) & dev::lds_u32(d1 + go.z) & m1) != 0u);
-            a.w = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + ro.w) & dev::lds_u32(d0 + go.w) & m0) != 0u);
-            b.w = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + ro.w) & dev::lds_u32(d1 + go.w) & m1) != 0u);
-            if (lane == 0) {
-              *reinterpret_cast<uint4*>(&cs.nz[0][wbase + j]) = a;
-              *reinterpret_cast<uint4*>(&cs.nz[1][wbase + j]) = b;
+          // runs of one group: the run's DD words once, then per episode
+          // its last type's row (offset by shuffle) AND DD and a ballot
+          uint32_t* nz0 = &cs.nz[0][wbase];
+          uint32_t* nz1 = &cs.nz[1][wbase];
+          for (uint32_t sm = segmask; sm;) {
+            const int s0 = __ffs(sm) - 1;
+            sm &= sm - 1u;
+            const int s1 = sm ? __ffs(sm) - 1 : nact;
+            const uint32_t go = __shfl_sync(0xffffffffu, my_go, s0);
+            const uint32_t dA = dev::lds_u32(d0 + go) & m0;
+            const uint32_t dB = dev::lds_u32(d1 + go) & m1;
+            int j = s0;
+            for (; j + 1 < s1; j += 2) {
+              const uint32_t r0 = __shfl_sync(0xffffffffu, my_ro, j);
+              const uint32_t r1 = __shfl_sync(0xffffffffu, my_ro, j + 1);
+              const uint32_t a0 = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + r0) & dA) != 0u);
+              const uint32_t b0 = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + r0) & dB) != 0u);
+              const uint32_t a1 = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + r1) & dA) != 0u);
+              const uint32_t b1 = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + r1) & dB) != 0u);
+              if (lane == 0) {
+                nz0[j] = a0;
+                nz1[j] = b0;
+                nz0[j + 1] = a1;
+                nz1[j + 1] = b1;
+              }
+            }
+            if (j < s1) {
+              const uint32_t r0 = __shfl_sync(0xffffffffu, my_ro, j);
+              const uint32_t a0 = __ballot_sync(0xffffffffu, (dev::lds_u32(l0 + r0) & dA) != 0u);
+              const uint32_t b0 = __ballot_sync(0xffffffffu, (dev::lds_u32(l1 + r0) & dB) != 0u);
+              if (lane == 0) {
+                nz0[j] = a0;
+                nz1[j] = b0;
+              }
             }
           }
           __syncwarp();
