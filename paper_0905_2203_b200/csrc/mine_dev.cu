@@ -1746,8 +1746,9 @@ void Engine::mine(const epi_mine_config& cfg, epi_mine_result* out, const epi_sh
         counts_all = d_all;
       }
       // threshold + compaction in candidate order, straight to host memory
-      if (surv.slot >= 0 && !std::getenv("EPI_SURV_TC")) {
-        // only pass-1 survivors can be frequent: compact those (in order)
+      if (surv.slot >= 0 && n <= kOneBlkMax && !std::getenv("EPI_SURV_TC")) {
+        // only pass-1 survivors can be frequent: compact those (in order);
+        // one CTA while the level (a bound on its survivors) is small
         surv_compact_1blk<<<1, kOneBlk, 0, st_>>>(
             surv.counts, cfg.threshold, slot_ptr(surv.slot), L, surv.types, surv.win,
             reinterpret_cast<uint32_t*>(dm + o_ft), reinterpret_cast<uint32_t*>(dm + o_fw),

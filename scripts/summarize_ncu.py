@@ -110,5 +110,33 @@ def launches(path):
         print(f"{v:10.1f} {cnt[k]:8d} {share:>6s}  {k}")
 
 
+
+
+def lines(rep, top=40):
+    """Executed warp-instructions per CUDA source line (cuda,sass view)."""
+    src = ncu_csv(["-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"])
+    hi = next(i for i, r in enumerate(src) if "Instructions Executed" in r)
+    hdr = src[hi]
+    ix = hdr.index("Instructions Executed")
+    per = defaultdict(int)
+    cur = "?"
+    total = 0
+    for r in src[hi + 1:]:
+        if len(r) <= ix:
+            continue
+        txt = r[1] if len(r) > 1 else ""
+        v = r[ix].replace(",", "")
+        # cuda rows carry "file:line" style text; sass rows start with an opcode
+        if r[0] and not r[0].startswith("0x") and not v:
+            cur = txt.strip()[:100]
+            continue
+        if v.isdigit():
+            per[(r[0] if not r[0].startswith("0x") else "", cur)] += int(v)
+            total += int(v)
+    print(f"# executed warp-instructions per source line: {rep} (total {total})")
+    for (k, c), v in sorted(per.items(), key=lambda x: -x[1])[:top]:
+        print(f"{v:16d} {v / max(total, 1) * 100:5.1f}%  {k} {c}")
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"full": full, "launches": launches, "lines": lines}[sys.argv[1]](sys.argv[2])
