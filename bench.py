@@ -607,7 +607,8 @@ def cpu_baseline_for(args, types, times, alphabet):
     """One bounded CPU sample (~10-60 s of host work): up to 1,000 seeded
     candidates over the whole stream, fewer on the longest streams."""
     cores, model = cpu_info()
-    value, secs, sample, kind = cpu_leg(args, types, times, alphabet, 1)
+    steps = 1
+    value, secs, sample, kind = cpu_leg(args, types, times, alphabet, steps)
     return {"value": value, "unit": "episode-events/s", "cores": cores, "kind": kind,
             "sample": f"{sample}; {steps} step(s) in {secs:.1f} s", "cpu": model}
 

@@ -170,3 +170,19 @@ def test_reference_arm_candidates_equal_product_draws():
         eps = oracle.mt_episodes(seed, 200, nodes, alphabet, [(0, 5), (5, 10), (10, 15)])
         csr = random_episodes_csr(seed, 200, nodes, alphabet, [(0, 5), (5, 10), (10, 15)])
         assert [csr.episode(i) for i in range(200)] == [(list(t), [tuple(c) for c in cs]) for t, cs in eps]
+
+
+def test_bench_cpu_baseline_leg():
+    """bench.py's cpu_baseline object (rank 0, N=1) on the cfg1 workload:
+    the reference timed on host cores, with the fields the contract names."""
+    import argparse
+    import sys
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    sys.path.insert(0, ROOT)
+    import bench
+    types, times, alphabet = bench.make_stream("cfg1")
+    args = argparse.Namespace(config="cfg1", cfg5_events=10_000_000, cfg5_cands=1_000_000)
+    cb = bench.cpu_baseline_for(args, types, times, alphabet)
+    assert cb["value"] > 0 and cb["cores"] >= 1 and cb["kind"] == "reference"
+    assert "1 step(s)" in cb["sample"] and cb["unit"] == "episode-events/s"
