@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(kMachThreads) chain_kernel(const CountLaunch p
   // run heads (segmask) let phase B load each run's DD word once
   const uint32_t my_go = static_cast<uint32_t>(grp > 0 ? grp : 0) * kRowStride * 4u;
   const uint32_t my_ro = ep.type[N - 1] * kRowStride * 4u;
-  const uint32_t segmask =
-      __ballot_sync(0xffffffffu, active && (lane == 0 || __shfl_up_sync(0xffffffffu, my_go, 1) != my_go));
+  // (the shuffle runs on every lane: a full-mask shuffle inside the
+  // short-circuit below would leave lanes out of the exchange)
+  const uint32_t prev_go = __shfl_up_sync(0xffffffffu, my_go, 1);
+  const uint32_t segmask = __ballot_sync(0xffffffffu, active && (lane == 0 || prev_go != my_go));
   if (dsel == M) {
     cs.erow[tid] = my_ro;
     cs.egrp[tid] = my_go;
