@@ -15,9 +15,9 @@
 // of (low + 1), the longest and shortest chain spans). Hence, after pe:
 //   * U_{N-1} bits in (pe, pe + L] are never completions;
 //   * bits after pe + sigma always are (the first one is the next completion);
-//   * a bit in (pe + L, pe + sigma] is decided by the exact automaton
-//     (tile_step of count_impl.cuh, cleared at pe), run until it is quiet - its
-//     last clear more than sigma before a tile boundary.
+//   * a bit in (pe + L, pe + sigma] is decided exactly by rebuilding the
+//     chain bitmaps from starts after pe over those few tiles
+//     (chain_validate).
 // The bulk of the work is a pure bitmap AND/dilate chain plus an "any bit"
 // test, with no automaton state, masks or clears.
 //
@@ -97,35 +97,48 @@ __device__ __forceinline__ void chain_record(const ChainCtx<N, W>& x, ChainState
   }
 }
 
-// The exact automaton cleared at s.pe, from pe's tile until quiet (or the
-// segment end); every completion is recorded.
+// The next completion after s.pe, when a chain end falls in (pe + L, pe + sigma]:
+// run_fsm cleared at pe holds, at position k, exactly the ends of chains of
+// the first k+1 nodes that start after pe (E/fsm.hpp:66-68, 83-91), so its
+// next completion is the first bit of U'_{N-1}, the chain bitmaps rebuilt
+// with U'_0 = occ(tau_0) restricted to (pe, inf). Any chain ending after
+// pe + sigma starts after pe, so only tiles up to pe + sigma are rebuilt
+// (at most 1 + sigma/32 tiles; the segment's tiles only). One completion per
+// call: the caller's greedy continues from it.
 template <int N, int W>
 __device__ __forceinline__ void chain_validate(const ChainCtx<N, W>& x, ChainState& s) {
-  using Hist = NarrowHist<N, W, true>;
-  const int64_t pe = x.T0 + s.pe;
-  const int32_t sigma = static_cast<int32_t>(x.ep.sigma);
-  Machine<N, Hist> m;
-  int32_t g = static_cast<int32_t>(pe >> 5);
-  m.hist.reset(g, 0);
-  m.set_threshold(pe);
-  int32_t lastc = s.pe;
-  auto on_c = [&](uint64_t tc) -> bool {
-    const int32_t t = static_cast<int32_t>(static_cast<int64_t>(tc) - x.T0);
-    chain_record(x, s, t);
-    lastc = t;
-    return false;
-  };
-  const int32_t g_first = g;
-  for (; g < x.gend; ++g) {
-    if (g > g_first && lastc + sigma < 32 * (g - x.g0)) break;
-    uint32_t occ[N];
+  const int64_t start = x.T0 + s.pe + 1;  // first admissible chain start (absolute ms)
+  const int64_t lim = x.T0 + s.pe + static_cast<int64_t>(x.ep.sigma);
+  int32_t g = static_cast<int32_t>(start >> 5);
+  const int32_t gl = static_cast<int32_t>(lim >> 5) + 1 < x.gend ? static_cast<int32_t>(lim >> 5) + 1 : x.gend;
+  uint32_t h[N > 1 ? N - 1 : 1];
 #pragma unroll
-    for (int k = 0; k < N; ++k) occ[k] = __ldg(x.p.occ + occ_index(g, x.ep.type[k], x.p.blk_words));
-    tile_step<N, Hist, true>(m, x.ep, occ, g, x.p, on_c);
+  for (int k = 0; k < N - 1; ++k) h[k] = 0;
+  uint32_t u0mask = ~0u << (start & 31);
+  for (; g < gl; ++g) {
+    uint32_t cw = __ldg(x.p.occ + occ_index(g, x.ep.type[0], x.p.blk_words)) & u0mask;
+    u0mask = ~0u;
+#pragma unroll
+    for (int k = 1; k < N; ++k) {
+      const uint32_t hi = x.ep.hi[k - 1];
+      const uint32_t o = __ldg(x.p.occ + occ_index(g, x.ep.type[k], x.p.blk_words));
+      const uint32_t nx = o & window_any<W, true>(cw, h[k - 1], 0u, hi - W + 1, hi);
+      h[k - 1] = cw;
+      cw = nx;
+    }
+    if (cw) {
+      const int32_t t = 32 * (g - x.g0) + (__ffs(cw) - 1);
+      chain_record(x, s, t);
+      s.pe = t;
+      s.floor = t + x.lsum;
+      s.ready = t + static_cast<int32_t>(x.ep.sigma);
+      return;
+    }
   }
-  s.pe = lastc;
-  s.floor = 32 * (g - x.g0) - 1;
-  s.ready = lastc + sigma;
+  // no chain from after pe ends by pe + sigma: the first chain end after it
+  // is the next completion
+  s.floor = s.pe + static_cast<int32_t>(x.ep.sigma);
+  s.ready = s.floor;
 }
 
 // Completions among the chain ends of one tile word (tile base `base`,
